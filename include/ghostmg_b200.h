@@ -1,0 +1,141 @@
+/*
+ * ghostmg_b200.h -- C ABI of the B200-native ghost-point multigrid V-cycle.
+ *
+ * The reference (arXiv 2207.14208 artifact `ghostmg`, pure Python) has no
+ * FFI; its drop-in seam is the Python solver object.  Each entry point
+ * below replaces one piece of that object, cited as
+ *   ref: /root/reference/pkg/src/ghostmg/<file>:<lines>
+ * The Python host layer (paper_2207_14208_b200/solver.py) binds these with
+ * ctypes and keeps the reference's build_solver / solve / measure_rho API.
+ *
+ * Conventions: plain pointers and sizes only; host arrays are read/written
+ * synchronously unless stated; device memory is owned by the context.
+ * Every int-returning call returns 0 on success and a negative code on
+ * failure, with a message in gmg_last_error().  Grid arrays are flat
+ * C-order (N+1)^d float64 like the reference (geometry.py:91-111); ghost
+ * vectors follow the ascending ghost order (geometry.py:416).
+ */
+#ifndef GHOSTMG_B200_H
+#define GHOSTMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gmg_ctx gmg_ctx;
+
+/* Coarsest-level direct solve supplied by the host (the reference's SciPy
+ * SuperLU object, ref solver.py:146-166): solve A x = rhs for the active
+ * unknowns (internal then ghost).  Return 0 on success. */
+typedef int (*gmg_coarse_cb)(void *user, int64_t n, const double *rhs, double *x);
+
+/* vector selectors for gmg_set_vector / gmg_get_vector / gmg_device_pointer */
+enum gmg_vector {
+  GMG_U = 0,      /* iterate / coarse error, full grid                      */
+  GMG_F = 1,      /* interior right-hand side, full grid                    */
+  GMG_G = 2,      /* ghost-row right-hand side, ascending ghost order       */
+  GMG_R_INT = 3,  /* interior residual scratch, full grid                   */
+  GMG_R_EXT = 4   /* ghost residual + band extension scratch, full grid     */
+};
+
+/* single-operation hooks for gmg_apply (parity tests, profiling) */
+enum gmg_op {
+  GMG_OP_GS_SWEEP = 0,       /* ref smoothing.py:127-132 gs_lex_sweep        */
+  GMG_OP_GHOST_SWEEP = 1,    /* ref smoothing.py:135-142 ghost_relax_sweep   */
+  GMG_OP_SMOOTH = 2,         /* ref smoothing.py:145-149 smooth(count)       */
+  GMG_OP_RES_INT = 3,        /* ref smoothing.py:111-118 -> GMG_R_INT        */
+  GMG_OP_RES_GHOST = 4,      /* ref smoothing.py:120-124 -> GMG_R_EXT ghosts */
+  GMG_OP_EXTEND_REXT = 5,    /* ref transfer.py:241-252 on GMG_R_EXT         */
+  GMG_OP_EXTEND_U = 6,       /* ref transfer.py:241-252 on GMG_U             */
+  GMG_OP_RESTRICT_INT = 7,   /* ref transfer.py:88-93  R_INT(l) -> F(l+1)    */
+  GMG_OP_RESTRICT_GHOST = 8, /* ref transfer.py:116-121 R_EXT(l) -> G(l+1)   */
+  GMG_OP_INTERP_ADD = 9,     /* ref transfer.py:149-151 + solver.py:198      */
+  GMG_OP_ZERO_U = 10
+};
+
+/* Library version (major*10000 + minor*100 + patch). */
+int gmg_version(void);
+
+/* Create a context for `nlevels` grid levels of dimension `ndim` (2 or 3)
+ * on CUDA device `device`.  Replaces MultigridSolver.__init__'s per-level
+ * plan construction (ref solver.py:103-127).  NULL on failure. */
+gmg_ctx *gmg_create(int device, int ndim, int nlevels);
+void gmg_destroy(gmg_ctx *ctx);
+const char *gmg_last_error(const gmg_ctx *ctx);
+
+/* Launch on a caller-owned cudaStream_t (e.g. torch's current stream);
+ * NULL restores the context's own stream. */
+int gmg_set_stream(gmg_ctx *ctx, void *cuda_stream);
+
+/* Upload one level: labels (ref geometry.py:374-431), ghost rows
+ * (ref operators.py:73-96, smoothing.py:50-77, 80-109: block low corner,
+ * 3^d weights, dtau, promotion flag), the order-equivalent ghost sweep
+ * batches, and the band plan (ref transfer.py:154-239: BFS group lengths,
+ * band nodes, neighbour masks, upwind steps, |n|). */
+int gmg_set_level(gmg_ctx *ctx, int level, int64_t N, double reaction,
+                  const uint8_t *labels, int64_t n_ghost, const int64_t *ghost_idx,
+                  const int64_t *ghost_low, const double *ghost_w,
+                  const double *ghost_dtau, const uint8_t *ghost_promoted,
+                  const int32_t *ghost_batch, int n_groups, const int64_t *bfs_len,
+                  const int64_t *band_idx, const uint8_t *bfs_mask,
+                  const int8_t *trans_step, const double *trans_absn);
+
+/* Cycle parameters (ref smoothing.py:30-47 SmootherConfig, solver.py:49-69
+ * CycleConfig): nu1, nu2, gamma (1 = V, 2 = W), coarse_mode (0 = host
+ * callback direct solve, 1 = `coarse_sweeps` smoothing sweeps), norm
+ * (0 = inf, 1 = l2). */
+int gmg_set_cycle(gmg_ctx *ctx, int nu1, int nu2, int gamma, int coarse_mode,
+                  int coarse_sweeps, int norm);
+int gmg_set_coarse_callback(gmg_ctx *ctx, gmg_coarse_cb cb, void *user);
+
+/* Host <-> device copies of a level vector (see enum gmg_vector). */
+int gmg_set_vector(gmg_ctx *ctx, int level, int which, const double *host);
+int gmg_get_vector(gmg_ctx *ctx, int level, int which, double *host);
+/* Device address of a level vector (valid for the context's lifetime). */
+void *gmg_device_pointer(gmg_ctx *ctx, int level, int which);
+
+/* Run one operation on a level (see enum gmg_op). */
+int gmg_apply(gmg_ctx *ctx, int level, int op, int count);
+
+/* Run `ncycles` cycles on level 0 in place (ref solver.py:170-203
+ * _cycle/run_cycle).  Asynchronous on the context stream except for the
+ * host coarse callback, which synchronizes. */
+int gmg_cycle(gmg_ctx *ctx, int ncycles);
+
+/* Residual norms of a level (ref solver.py:135-142): out[0] = max |r_int|,
+ * out[1] = max |r_ghost| (norm = inf), or out[0] = sum r_int^2 and
+ * out[1] = sum r_ghost^2 in NumPy's pairwise order (norm = l2).
+ * Synchronizes. */
+int gmg_residual_norm(gmg_ctx *ctx, int level, double *out);
+
+/* peak = max |u| on level 0; if 0 < peak < threshold, u *= factor and
+ * *scaled = 1 (ref solver.py:239-243).  Synchronizes. */
+int gmg_abs_max_scale(gmg_ctx *ctx, double threshold, double factor, double *peak,
+                      int *scaled);
+
+int gmg_synchronize(gmg_ctx *ctx);
+
+/* Kernels launched by this context so far. */
+int64_t gmg_launch_count(const gmg_ctx *ctx);
+/* Device bytes held by the context. */
+int64_t gmg_device_bytes(const gmg_ctx *ctx);
+
+/* Per-kernel-class CUDA-event timing (0 gs sweep, 1 ghost sweep,
+ * 2 residuals, 3 band, 4 restriction, 5 interpolation, 6 coarse solve,
+ * 7 norms).  gmg_profile(ctx, 1) starts recording, gmg_profile_read
+ * synchronizes and returns the summed milliseconds and launch count. */
+int gmg_profile(gmg_ctx *ctx, int enable);
+int gmg_profile_read(gmg_ctx *ctx, int kclass, double *total_ms, int64_t *count);
+
+/* Host helper: n draws of the reference's xorshift64* stream from (-1, 1)
+ * (ref rng.py:14-56 uniform_symmetric), written to out. */
+int gmg_uniform_symmetric(uint64_t seed, int64_t n, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GHOSTMG_B200_H */

@@ -1,0 +1,210 @@
+"""ctypes binding of libghostmg_b200.so (include/ghostmg_b200.h).
+
+The library is the product path: there is no Python or CPU fallback for any
+cycle operation.  Importing works without a GPU (so the exported ABI can be
+checked on CPU); creating a context without a CUDA device raises.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libghostmg_b200.so")
+HEADER = os.path.join(HERE, "..", "include", "ghostmg_b200.h")
+
+U, F, G, R_INT, R_EXT = 0, 1, 2, 3, 4
+OP_GS_SWEEP, OP_GHOST_SWEEP, OP_SMOOTH, OP_RES_INT, OP_RES_GHOST = 0, 1, 2, 3, 4
+OP_EXTEND_REXT, OP_EXTEND_U, OP_RESTRICT_INT, OP_RESTRICT_GHOST, OP_INTERP_ADD, OP_ZERO_U = 5, 6, 7, 8, 9, 10
+KCLASS = {"gs_sweep": 0, "ghost_sweep": 1, "residual": 2, "band": 3, "restrict": 4,
+          "interp": 5, "coarse": 6, "norm": 7}
+
+_p = ctypes.c_void_p
+_i = ctypes.c_int
+_i64 = ctypes.c_int64
+_d = ctypes.c_double
+
+COARSE_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                             ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double))
+
+SIGNATURES = {
+    "gmg_version": (_i, []),
+    "gmg_create": (_p, [_i, _i, _i]),
+    "gmg_destroy": (None, [_p]),
+    "gmg_last_error": (ctypes.c_char_p, [_p]),
+    "gmg_set_stream": (_i, [_p, _p]),
+    "gmg_set_level": (_i, [_p, _i, _i64, _d, _p, _i64, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p]),
+    "gmg_set_cycle": (_i, [_p, _i, _i, _i, _i, _i, _i]),
+    "gmg_set_coarse_callback": (_i, [_p, COARSE_CB, _p]),
+    "gmg_set_vector": (_i, [_p, _i, _i, _p]),
+    "gmg_get_vector": (_i, [_p, _i, _i, _p]),
+    "gmg_device_pointer": (_p, [_p, _i, _i]),
+    "gmg_apply": (_i, [_p, _i, _i, _i]),
+    "gmg_cycle": (_i, [_p, _i]),
+    "gmg_residual_norm": (_i, [_p, _i, _p]),
+    "gmg_abs_max_scale": (_i, [_p, _d, _d, _p, _p]),
+    "gmg_synchronize": (_i, [_p]),
+    "gmg_launch_count": (_i64, [_p]),
+    "gmg_device_bytes": (_i64, [_p]),
+    "gmg_profile": (_i, [_p, _i]),
+    "gmg_profile_read": (_i, [_p, _i, _p, _p]),
+    "gmg_uniform_symmetric": (_i, [ctypes.c_uint64, _i64, _p]),
+}
+
+_lib = None
+
+
+def load():
+    """Load (building first if the sources are newer) the CUDA library."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    from . import _build
+    if _build.needs_build():
+        _build.build()
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing; run __graft_entry__.build()")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None and a.size else None
+
+
+class GmgError(RuntimeError):
+    pass
+
+
+class Context:
+    """Owner of one gmg_ctx (device buffers of a whole hierarchy)."""
+
+    def __init__(self, ndim, nlevels, device=0):
+        self.lib = load()
+        self.ctx = self.lib.gmg_create(device, ndim, nlevels)
+        if not self.ctx:
+            raise GmgError("gmg_create failed: no usable CUDA device "
+                           "(the B200 path has no CPU fallback)")
+        self.nlevels = nlevels
+        self._keep = []
+
+    def check(self, rc):
+        if rc != 0:
+            msg = self.lib.gmg_last_error(self.ctx)
+            raise GmgError(msg.decode() if msg else f"gmg error {rc}")
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.gmg_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- upload ---------------------------------------------------------
+    def set_level(self, level, plan):
+        c = np.ascontiguousarray
+        self._lvl_arrays = arr = dict(
+            labels=c(plan.labels, np.uint8), gi=c(plan.ghost_idx, np.int64),
+            glow=c(plan.ghost_low, np.int64), gw=c(plan.ghost_w, np.float64),
+            gdt=c(plan.ghost_dtau, np.float64), gpr=c(plan.ghost_promoted, np.uint8),
+            gb=c(plan.ghost_batch, np.int32), bl=c(plan.bfs_len, np.int64),
+            bi=c(plan.band_idx, np.int64), bm=c(plan.bfs_mask, np.uint8),
+            ts=c(plan.trans_step, np.int8), ta=c(plan.trans_absn, np.float64))
+        self.check(self.lib.gmg_set_level(
+            self.ctx, level, plan.N, float(plan.reaction), ptr(arr["labels"]), plan.n_ghosts,
+            ptr(arr["gi"]), ptr(arr["glow"]), ptr(arr["gw"]), ptr(arr["gdt"]), ptr(arr["gpr"]),
+            ptr(arr["gb"]), len(arr["bl"]), ptr(arr["bl"]), ptr(arr["bi"]), ptr(arr["bm"]),
+            ptr(arr["ts"]), ptr(arr["ta"])))
+        del self._lvl_arrays
+
+    def set_cycle(self, nu1, nu2, gamma, coarse_mode, coarse_sweeps, norm):
+        self.check(self.lib.gmg_set_cycle(self.ctx, nu1, nu2, gamma, coarse_mode, coarse_sweeps, norm))
+
+    def set_coarse_callback(self, fn):
+        """fn(rhs ndarray) -> solution ndarray."""
+
+        def trampoline(user, n, rhs, x):
+            try:
+                r = np.ctypeslib.as_array(rhs, shape=(n,)).copy()
+                out = np.ctypeslib.as_array(x, shape=(n,))
+                out[:] = fn(r)
+                return 0
+            except Exception:  # propagate as an error code
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        cb = COARSE_CB(trampoline)
+        self._keep.append(cb)
+        self.check(self.lib.gmg_set_coarse_callback(self.ctx, cb, None))
+
+    def set_stream(self, stream_handle):
+        self.check(self.lib.gmg_set_stream(self.ctx, stream_handle))
+
+    # -- vectors --------------------------------------------------------
+    def set_vector(self, level, which, host):
+        host = np.ascontiguousarray(host, dtype=np.float64)
+        self.check(self.lib.gmg_set_vector(self.ctx, level, which, ptr(host)))
+
+    def get_vector(self, level, which, n):
+        out = np.empty(n, dtype=np.float64)
+        if n:
+            self.check(self.lib.gmg_get_vector(self.ctx, level, which, ptr(out)))
+        return out
+
+    def device_pointer(self, level, which):
+        return self.lib.gmg_device_pointer(self.ctx, level, which)
+
+    def apply(self, level, op, count=1):
+        self.check(self.lib.gmg_apply(self.ctx, level, op, count))
+
+    def cycle(self, n=1):
+        self.check(self.lib.gmg_cycle(self.ctx, n))
+
+    def residual_parts(self, level=0):
+        out = np.zeros(2)
+        self.check(self.lib.gmg_residual_norm(self.ctx, level, ptr(out)))
+        return float(out[0]), float(out[1])
+
+    def abs_max_scale(self, threshold=1e-250, factor=1e250):
+        peak = np.zeros(1)
+        scaled = np.zeros(1, dtype=np.int32)
+        self.check(self.lib.gmg_abs_max_scale(self.ctx, threshold, factor, ptr(peak), ptr(scaled)))
+        return float(peak[0]), bool(scaled[0])
+
+    def synchronize(self):
+        self.check(self.lib.gmg_synchronize(self.ctx))
+
+    @property
+    def launches(self):
+        return int(self.lib.gmg_launch_count(self.ctx))
+
+    @property
+    def device_bytes(self):
+        return int(self.lib.gmg_device_bytes(self.ctx))
+
+    def profile(self, enable=True):
+        self.check(self.lib.gmg_profile(self.ctx, 1 if enable else 0))
+
+    def profile_read(self, kclass):
+        ms = np.zeros(1)
+        cnt = np.zeros(1, dtype=np.int64)
+        self.check(self.lib.gmg_profile_read(self.ctx, KCLASS.get(kclass, kclass), ptr(ms), ptr(cnt)))
+        return float(ms[0]), int(cnt[0])
+
+
+def uniform_symmetric_native(seed, n):
+    out = np.empty(int(n), dtype=np.float64)
+    if n:
+        load().gmg_uniform_symmetric(int(seed) & ((1 << 64) - 1), int(n), ptr(out))
+    return out

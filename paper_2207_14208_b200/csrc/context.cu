@@ -1,0 +1,738 @@
+// context.cu -- device context, level upload, the V/W-cycle driver and the
+// C ABI (include/ghostmg_b200.h).
+//
+// The cycle driver restates MultigridSolver._cycle
+// (/root/reference/pkg/src/ghostmg/solver.py:170-199) as a stream of kernel
+// launches: nu1 smoothing steps, interior + ghost residual, band
+// extension of the ghost residual, both restrictions, recursion (or the
+// coarsest solve), band extension of the coarse error, interpolation +
+// correction, nu2 smoothing steps.  Nothing leaves the device except the
+// coarsest right-hand side when the host SuperLU callback is used.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ghostmg_b200.h"
+#include "gmg_kernels.cuh"
+
+using namespace gmg;
+
+namespace {
+
+struct DevLevel {
+  Geom g{};
+  int d = 0;
+  int64_t N = 0;
+  uint8_t* labels = nullptr;
+  double *u = nullptr, *f = nullptr, *rI = nullptr, *rE = nullptr;
+  // ghosts, slot order
+  int64_t ng = 0;
+  int64_t *gnode = nullptr, *gbase = nullptr;
+  double *gw = nullptr, *gdtau = nullptr, *gval = nullptr, *gtmp = nullptr;
+  uint8_t* gprom = nullptr;
+  int32_t *slot2lex = nullptr, *lex2slot = nullptr;
+  std::vector<int64_t> batch_off;  // slot offsets of sweep batches
+  // band
+  int64_t nb = 0;
+  int64_t* band_idx = nullptr;
+  uint8_t* bfs_mask = nullptr;
+  int8_t* tstep = nullptr;
+  double *tabsn = nullptr, *bscratch = nullptr;
+  std::vector<int64_t> bfs_off;
+  // Gauss-Seidel tasks
+  int2* tasks = nullptr;
+  int ntasks = 0, B1 = 1, Bn = 1, C = 1;
+  int *progress = nullptr, *ticket = nullptr;
+  // coarsest direct solve
+  int64_t n_int = 0;
+  int64_t* active = nullptr;  // internal nodes then ghost nodes (lex)
+  double *rhs_d = nullptr, *x_d = nullptr, *rhs_h = nullptr, *x_h = nullptr;
+  bool ready = false;
+};
+
+struct Prof {
+  cudaEvent_t a, b;
+  int cls;
+};
+
+}  // namespace
+
+struct gmg_ctx {
+  int device = 0;
+  int ndim = 0;
+  int nlevels = 0;
+  std::vector<DevLevel> L;
+  cudaStream_t own = nullptr, stream = nullptr;
+  int nu1 = 2, nu2 = 1, gamma = 1, coarse_mode = 0, coarse_sweeps = 500, norm = 0;
+  gmg_coarse_cb cb = nullptr;
+  void* cb_user = nullptr;
+  unsigned long long* dmax = nullptr;  // reduction slots
+  unsigned long long* hmax = nullptr;  // pinned mirror
+  std::string err;
+  int64_t launches = 0;
+  int64_t bytes = 0;
+  bool prof = false;
+  std::vector<Prof> events;
+  std::vector<cudaEvent_t> pool;
+};
+
+namespace {
+
+#define GMG_CHECK(ctx, call)                                                         \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      (ctx)->err = std::string(#call) + ": " + cudaGetErrorString(e_);               \
+      return -1;                                                                     \
+    }                                                                                \
+  } while (0)
+
+int fail(gmg_ctx* ctx, const std::string& m) {
+  if (ctx) ctx->err = m;
+  return -2;
+}
+
+template <class T>
+int dalloc(gmg_ctx* ctx, T** p, int64_t count) {
+  *p = nullptr;
+  if (count <= 0) return 0;
+  cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (size_t)count);
+  if (e != cudaSuccess) {
+    ctx->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+    return -1;
+  }
+  ctx->bytes += (int64_t)sizeof(T) * count;
+  return 0;
+}
+
+template <class T>
+int upload(gmg_ctx* ctx, T** p, const T* host, int64_t count) {
+  if (dalloc(ctx, p, count)) return -1;
+  if (count > 0) GMG_CHECK(ctx, cudaMemcpy(*p, host, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+void free_level(DevLevel& l) {
+  void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
+                  l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
+                  l.bscratch, l.tasks, l.progress, l.ticket, l.active, l.rhs_d, l.x_d};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (l.rhs_h) cudaFreeHost(l.rhs_h);
+  if (l.x_h) cudaFreeHost(l.x_h);
+  l = DevLevel();
+}
+
+// ---- profiling ----------------------------------------------------------
+struct Scope {
+  gmg_ctx* ctx;
+  int cls;
+  cudaEvent_t a = nullptr;
+  Scope(gmg_ctx* c, int k) : ctx(c), cls(k) {
+    if (!ctx->prof) return;
+    a = take();
+    cudaEventRecord(a, ctx->stream);
+  }
+  cudaEvent_t take() {
+    if (ctx->pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = ctx->pool.back();
+    ctx->pool.pop_back();
+    return e;
+  }
+  ~Scope() {
+    if (!ctx->prof) return;
+    cudaEvent_t b = take();
+    cudaEventRecord(b, ctx->stream);
+    ctx->events.push_back({a, b, cls});
+  }
+};
+
+// ---- level helpers ---------------------------------------------------------
+Geom make_geom(int d, int64_t N, double reaction) {
+  Geom g{};
+  g.d = d;
+  g.N = N;
+  g.n = N + 1;
+  if (d == 3) {
+    g.s0 = g.n * g.n;
+    g.s1 = g.n;
+    g.s2 = 1;
+    g.nodes = g.n * g.n * g.n;
+  } else {
+    g.s0 = g.n;
+    g.s1 = 1;
+    g.s2 = 0;
+    g.nodes = g.n * g.n;
+  }
+  const double h = 2.0 / (double)N;
+  g.h2 = h * h;  // Python h**2 == h*h (correctly rounded square)
+  g.denom = 2.0 * d + reaction * g.h2;
+  g.inv = 1.0 / g.denom;
+  g.c = g.denom / g.h2;
+  return g;
+}
+
+GhostArgs ghost_args(const DevLevel& l) {
+  GhostArgs a;
+  a.g = l.g;
+  a.ng = l.ng;
+  a.node = l.gnode;
+  a.base = l.gbase;
+  a.w = l.gw;
+  a.dtau = l.gdtau;
+  a.gval = l.gval;
+  a.promoted = l.gprom;
+  return a;
+}
+
+BandArgs band_args(const DevLevel& l) {
+  BandArgs a;
+  a.g = l.g;
+  a.nb = l.nb;
+  a.idx = l.band_idx;
+  a.mask = l.bfs_mask;
+  a.step = l.tstep;
+  a.absn = l.tabsn;
+  a.scratch = l.bscratch;
+  return a;
+}
+
+int gs_grid(const DevLevel& l) {
+  int warps = std::min(l.ntasks, 148 * 16);
+  return std::max(1, (warps + 3) / 4);
+}
+
+// ---- operations ------------------------------------------------------------
+int op_gs(gmg_ctx* ctx, DevLevel& l) {
+  Scope s(ctx, 0);
+  GMG_CHECK(ctx, cudaMemsetAsync(l.progress, 0, sizeof(int) * (size_t)(l.C * l.Bn + 1), ctx->stream));
+  GsArgs a;
+  a.g = l.g;
+  a.labels = l.labels;
+  a.u = l.u;
+  a.f = l.f;
+  a.tasks = l.tasks;
+  a.ntasks = l.ntasks;
+  a.ticket = l.ticket;
+  a.progress = l.progress;
+  a.B1 = l.B1;
+  a.Bn = l.Bn;
+  a.C = l.C;
+  launch_gs_sweep(a, gs_grid(l), ctx->stream);
+  ctx->launches++;
+  return 0;
+}
+
+int op_ghost_sweep(gmg_ctx* ctx, DevLevel& l) {
+  Scope s(ctx, 1);
+  GhostArgs a = ghost_args(l);
+  for (size_t b = 0; b + 1 < l.batch_off.size(); ++b) {
+    launch_ghost_batch(a, l.u, l.batch_off[b], l.batch_off[b + 1], ctx->stream);
+    ctx->launches++;
+  }
+  return 0;
+}
+
+int op_smooth(gmg_ctx* ctx, DevLevel& l, int count) {
+  for (int i = 0; i < count; ++i) {
+    if (op_gs(ctx, l)) return -1;
+    if (op_ghost_sweep(ctx, l)) return -1;
+  }
+  return 0;
+}
+
+int op_res_int(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
+  Scope s(ctx, slot ? 7 : 2);
+  launch_residual_interior(l.g, l.labels, l.u, l.f, l.rI, slot, ctx->stream);
+  ctx->launches++;
+  return 0;
+}
+
+int op_res_ghost(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
+  if (l.ng == 0) return 0;
+  Scope s(ctx, slot ? 7 : 2);
+  launch_residual_ghost(ghost_args(l), l.u, l.rE, slot, ctx->stream);
+  ctx->launches++;
+  return 0;
+}
+
+int op_extend(gmg_ctx* ctx, DevLevel& l, double* x) {
+  if (l.nb == 0) return 0;
+  Scope s(ctx, 3);
+  BandArgs a = band_args(l);
+  for (size_t gi = 0; gi + 1 < l.bfs_off.size(); ++gi) {
+    launch_band_bfs(a, x, l.bfs_off[gi], l.bfs_off[gi + 1], ctx->stream);
+    ctx->launches++;
+  }
+  launch_band_transport(a, x, ctx->stream);
+  ctx->launches += 12;
+  return 0;
+}
+
+int op_restrict_int(gmg_ctx* ctx, DevLevel& f, DevLevel& c) {
+  Scope s(ctx, 4);
+  launch_restrict_interior(f.g, f.labels, f.rI, c.g, c.labels, c.f, ctx->stream);
+  ctx->launches++;
+  return 0;
+}
+
+int op_restrict_ghost(gmg_ctx* ctx, DevLevel& f, DevLevel& c) {
+  if (c.ng == 0) return 0;
+  Scope s(ctx, 4);
+  launch_restrict_ghost(f.g, f.labels, f.rE, ghost_args(c), c.gval, ctx->stream);
+  ctx->launches++;
+  return 0;
+}
+
+int op_interp(gmg_ctx* ctx, DevLevel& f, DevLevel& c) {
+  Scope s(ctx, 5);
+  launch_interp_add(f.g, f.labels, f.u, c.g, c.u, ctx->stream);
+  ctx->launches++;
+  return 0;
+}
+
+int coarse_solve(gmg_ctx* ctx, int li) {
+  DevLevel& l = ctx->L[li];
+  Scope s(ctx, 6);
+  GMG_CHECK(ctx, cudaMemsetAsync(l.u, 0, sizeof(double) * (size_t)l.g.nodes, ctx->stream));
+  if (ctx->coarse_mode == 1) return op_smooth(ctx, l, ctx->coarse_sweeps);
+  if (!ctx->cb) return fail(ctx, "coarsest direct solve requested but no callback set");
+  const int64_t n = l.n_int + l.ng;
+  launch_gather(l.active, l.n_int, l.f, l.lex2slot, l.ng, l.gval, l.rhs_d, ctx->stream);
+  ctx->launches++;
+  GMG_CHECK(ctx, cudaMemcpyAsync(l.rhs_h, l.rhs_d, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->cb(ctx->cb_user, n, l.rhs_h, l.x_h) != 0) return fail(ctx, "coarse solve callback failed");
+  GMG_CHECK(ctx, cudaMemcpyAsync(l.x_d, l.x_h, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+  launch_scatter(l.active, n, l.x_d, l.u, ctx->stream);
+  ctx->launches++;
+  return 0;
+}
+
+int cycle_level(gmg_ctx* ctx, int li) {
+  DevLevel& l = ctx->L[li];
+  DevLevel& c = ctx->L[li + 1];
+  if (op_smooth(ctx, l, ctx->nu1)) return -1;
+  if (op_res_int(ctx, l, nullptr)) return -1;
+  if (op_res_ghost(ctx, l, nullptr)) return -1;
+  if (op_extend(ctx, l, l.rE)) return -1;
+  if (op_restrict_int(ctx, l, c)) return -1;
+  if (op_restrict_ghost(ctx, l, c)) return -1;
+  if (li + 1 == ctx->nlevels - 1) {
+    if (coarse_solve(ctx, li + 1)) return -1;
+  } else {
+    GMG_CHECK(ctx, cudaMemsetAsync(c.u, 0, sizeof(double) * (size_t)c.g.nodes, ctx->stream));
+    for (int k = 0; k < ctx->gamma; ++k)
+      if (cycle_level(ctx, li + 1)) return -1;
+  }
+  if (op_extend(ctx, c, c.u)) return -1;
+  if (op_interp(ctx, l, c)) return -1;
+  return op_smooth(ctx, l, ctx->nu2);
+}
+
+bool levels_ready(gmg_ctx* ctx) {
+  for (auto& l : ctx->L)
+    if (!l.ready) return false;
+  return true;
+}
+
+}  // namespace
+
+// =========================================================================
+extern "C" {
+
+int gmg_version(void) { return 100; }
+
+gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
+  if (ndim != 2 && ndim != 3) return nullptr;
+  if (nlevels < 2) return nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return nullptr;
+  gmg_ctx* ctx = new gmg_ctx();
+  ctx->device = device;
+  ctx->ndim = ndim;
+  ctx->nlevels = nlevels;
+  ctx->L.resize(nlevels);
+  if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return nullptr;
+  }
+  ctx->stream = ctx->own;
+  if (cudaMalloc(&ctx->dmax, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMallocHost(&ctx->hmax, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+    delete ctx;
+    return nullptr;
+  }
+  return ctx;
+}
+
+void gmg_destroy(gmg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& l : ctx->L) free_level(l);
+  for (auto& e : ctx->events) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : ctx->pool) cudaEventDestroy(e);
+  if (ctx->dmax) cudaFree(ctx->dmax);
+  if (ctx->hmax) cudaFreeHost(ctx->hmax);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+}
+
+const char* gmg_last_error(const gmg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int gmg_set_stream(gmg_ctx* ctx, void* s) {
+  ctx->stream = s ? (cudaStream_t)s : ctx->own;
+  return 0;
+}
+
+int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_t* labels,
+                  int64_t ng, const int64_t* ghost_idx, const int64_t* ghost_low,
+                  const double* ghost_w, const double* ghost_dtau, const uint8_t* ghost_promoted,
+                  const int32_t* ghost_batch, int n_groups, const int64_t* bfs_len,
+                  const int64_t* band_idx, const uint8_t* bfs_mask, const int8_t* trans_step,
+                  const double* trans_absn) {
+  if (li < 0 || li >= ctx->nlevels) return fail(ctx, "level out of range");
+  if (N < 2 || (N % 2)) return fail(ctx, "N must be even and >= 2");
+  cudaSetDevice(ctx->device);
+  DevLevel& l = ctx->L[li];
+  free_level(l);
+  const int d = ctx->ndim;
+  l.d = d;
+  l.N = N;
+  l.g = make_geom(d, N, reaction);
+  const int64_t nodes = l.g.nodes;
+  const int m = d == 3 ? 27 : 9;
+  if (upload(ctx, &l.labels, labels, nodes)) return -1;
+  if (dalloc(ctx, &l.u, nodes) || dalloc(ctx, &l.f, nodes) || dalloc(ctx, &l.rI, nodes) ||
+      dalloc(ctx, &l.rE, nodes))
+    return -1;
+  GMG_CHECK(ctx, cudaMemset(l.u, 0, sizeof(double) * nodes));
+  GMG_CHECK(ctx, cudaMemset(l.f, 0, sizeof(double) * nodes));
+  GMG_CHECK(ctx, cudaMemset(l.rI, 0, sizeof(double) * nodes));
+  GMG_CHECK(ctx, cudaMemset(l.rE, 0, sizeof(double) * nodes));
+
+  // ghosts -> slot order (stable by batch)
+  l.ng = ng;
+  if (ng > 0) {
+    int32_t maxb = 0;
+    for (int64_t i = 0; i < ng; ++i) maxb = std::max(maxb, ghost_batch[i]);
+    std::vector<int64_t> cnt(maxb + 2, 0);
+    for (int64_t i = 0; i < ng; ++i) cnt[ghost_batch[i] + 1]++;
+    for (int b = 0; b <= maxb; ++b) cnt[b + 1] += cnt[b];
+    l.batch_off.assign(cnt.begin(), cnt.end());
+    std::vector<int32_t> s2l(ng), l2s(ng);
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t i = 0; i < ng; ++i) {
+      int64_t s = fill[ghost_batch[i]]++;
+      s2l[s] = (int32_t)i;
+      l2s[i] = (int32_t)s;
+    }
+    std::vector<int64_t> node(ng), base(ng);
+    std::vector<double> w((size_t)m * ng), dt(ng);
+    std::vector<uint8_t> pr(ng);
+    const int64_t st[3] = {l.g.s0, l.g.s1, l.g.s2};
+    for (int64_t s = 0; s < ng; ++s) {
+      const int64_t i = s2l[s];
+      node[s] = ghost_idx[i];
+      int64_t b = 0;
+      for (int k = 0; k < d; ++k) b += ghost_low[i * d + k] * st[k];
+      base[s] = b;
+      for (int j = 0; j < m; ++j) w[(size_t)j * ng + s] = ghost_w[i * m + j];
+      dt[s] = ghost_dtau[i];
+      pr[s] = ghost_promoted[i];
+    }
+    if (upload(ctx, &l.gnode, node.data(), ng) || upload(ctx, &l.gbase, base.data(), ng) ||
+        upload(ctx, &l.gw, w.data(), (int64_t)m * ng) || upload(ctx, &l.gdtau, dt.data(), ng) ||
+        upload(ctx, &l.gprom, pr.data(), ng) || upload(ctx, &l.slot2lex, s2l.data(), ng) ||
+        upload(ctx, &l.lex2slot, l2s.data(), ng) || dalloc(ctx, &l.gval, ng) ||
+        dalloc(ctx, &l.gtmp, ng))
+      return -1;
+    GMG_CHECK(ctx, cudaMemset(l.gval, 0, sizeof(double) * ng));
+  } else {
+    l.batch_off.assign(1, 0);
+  }
+
+  // band
+  int64_t nb = 0;
+  l.bfs_off.assign(1, 0);
+  for (int gi = 0; gi < n_groups; ++gi) {
+    nb += bfs_len[gi];
+    l.bfs_off.push_back(nb);
+  }
+  l.nb = nb;
+  if (nb > 0) {
+    if (upload(ctx, &l.band_idx, band_idx, nb) || upload(ctx, &l.bfs_mask, bfs_mask, nb) ||
+        upload(ctx, &l.tstep, trans_step, nb * d) || upload(ctx, &l.tabsn, trans_absn, nb * d) ||
+        dalloc(ctx, &l.bscratch, nb))
+      return -1;
+  }
+
+  // Gauss-Seidel wavefront tasks
+  l.C = (int)((N - 1 + 31) / 32);
+  if (d == 3) {
+    l.B1 = N - 1 >= 512 ? 16 : 8;
+    l.Bn = (int)((N - 1 + l.B1 - 1) / l.B1);
+  } else {
+    l.B1 = 1;
+    l.Bn = 1;
+  }
+  std::vector<int2> tasks;
+  for (int s = 0; s <= l.C + l.Bn - 2; ++s)
+    for (int c = 0; c < l.C; ++c) {
+      const int b = s - c;
+      if (b >= 0 && b < l.Bn) tasks.push_back(make_int2(c, b));
+    }
+  l.ntasks = (int)tasks.size();
+  if (upload(ctx, &l.tasks, tasks.data(), l.ntasks) || dalloc(ctx, &l.progress, l.C * l.Bn + 1))
+    return -1;
+  l.ticket = l.progress + l.C * l.Bn;
+
+  // coarsest direct-solve ordering: internal then ghost (ref operators.py:180)
+  if (li == ctx->nlevels - 1) {
+    std::vector<int64_t> act;
+    for (int64_t i = 0; i < nodes; ++i)
+      if (labels[i] == INTERNAL) act.push_back(i);
+    l.n_int = (int64_t)act.size();
+    for (int64_t i = 0; i < ng; ++i) act.push_back(ghost_idx[i]);
+    const int64_t n = (int64_t)act.size();
+    if (upload(ctx, &l.active, act.data(), n) || dalloc(ctx, &l.rhs_d, n) || dalloc(ctx, &l.x_d, n))
+      return -1;
+    GMG_CHECK(ctx, cudaMallocHost(&l.rhs_h, sizeof(double) * (size_t)std::max<int64_t>(n, 1)));
+    GMG_CHECK(ctx, cudaMallocHost(&l.x_h, sizeof(double) * (size_t)std::max<int64_t>(n, 1)));
+  }
+  l.ready = true;
+  return 0;
+}
+
+int gmg_set_cycle(gmg_ctx* ctx, int nu1, int nu2, int gamma, int coarse_mode, int coarse_sweeps,
+                  int norm) {
+  if (nu1 < 0 || nu2 < 0 || nu1 + nu2 == 0) return fail(ctx, "need nu1, nu2 >= 0, not both 0");
+  if (gamma < 1) return fail(ctx, "gamma must be >= 1");
+  if (coarse_mode < 0 || coarse_mode > 1) return fail(ctx, "unknown coarse mode");
+  if (norm < 0 || norm > 1) return fail(ctx, "unknown norm");
+  ctx->nu1 = nu1;
+  ctx->nu2 = nu2;
+  ctx->gamma = gamma;
+  ctx->coarse_mode = coarse_mode;
+  ctx->coarse_sweeps = coarse_sweeps;
+  ctx->norm = norm;
+  return 0;
+}
+
+int gmg_set_coarse_callback(gmg_ctx* ctx, gmg_coarse_cb cb, void* user) {
+  ctx->cb = cb;
+  ctx->cb_user = user;
+  return 0;
+}
+
+static double* vec_ptr(DevLevel& l, int which) {
+  switch (which) {
+    case GMG_U: return l.u;
+    case GMG_F: return l.f;
+    case GMG_G: return l.gval;
+    case GMG_R_INT: return l.rI;
+    case GMG_R_EXT: return l.rE;
+  }
+  return nullptr;
+}
+
+int gmg_set_vector(gmg_ctx* ctx, int li, int which, const double* host) {
+  if (li < 0 || li >= ctx->nlevels || !ctx->L[li].ready) return fail(ctx, "level not set");
+  DevLevel& l = ctx->L[li];
+  cudaSetDevice(ctx->device);
+  if (which == GMG_G) {
+    if (l.ng == 0) return 0;
+    GMG_CHECK(ctx, cudaMemcpyAsync(l.gtmp, host, sizeof(double) * l.ng, cudaMemcpyHostToDevice, ctx->stream));
+    launch_permute(l.gtmp, l.slot2lex, l.ng, l.gval, ctx->stream);
+    ctx->launches++;
+    GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+    return 0;
+  }
+  double* p = vec_ptr(l, which);
+  if (!p) return fail(ctx, "unknown vector");
+  GMG_CHECK(ctx, cudaMemcpyAsync(p, host, sizeof(double) * l.g.nodes, cudaMemcpyHostToDevice, ctx->stream));
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int gmg_get_vector(gmg_ctx* ctx, int li, int which, double* host) {
+  if (li < 0 || li >= ctx->nlevels || !ctx->L[li].ready) return fail(ctx, "level not set");
+  DevLevel& l = ctx->L[li];
+  cudaSetDevice(ctx->device);
+  if (which == GMG_G) {
+    if (l.ng == 0) return 0;
+    launch_permute(l.gval, l.lex2slot, l.ng, l.gtmp, ctx->stream);
+    ctx->launches++;
+    GMG_CHECK(ctx, cudaMemcpyAsync(host, l.gtmp, sizeof(double) * l.ng, cudaMemcpyDeviceToHost, ctx->stream));
+    GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+    return 0;
+  }
+  double* p = vec_ptr(l, which);
+  if (!p) return fail(ctx, "unknown vector");
+  GMG_CHECK(ctx, cudaMemcpyAsync(host, p, sizeof(double) * l.g.nodes, cudaMemcpyDeviceToHost, ctx->stream));
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+void* gmg_device_pointer(gmg_ctx* ctx, int li, int which) {
+  if (li < 0 || li >= ctx->nlevels) return nullptr;
+  return vec_ptr(ctx->L[li], which);
+}
+
+int gmg_apply(gmg_ctx* ctx, int li, int op, int count) {
+  if (li < 0 || li >= ctx->nlevels || !ctx->L[li].ready) return fail(ctx, "level not set");
+  cudaSetDevice(ctx->device);
+  DevLevel& l = ctx->L[li];
+  const bool has_c = li + 1 < ctx->nlevels && ctx->L[li + 1].ready;
+  int rc = 0;
+  switch (op) {
+    case GMG_OP_GS_SWEEP: rc = op_gs(ctx, l); break;
+    case GMG_OP_GHOST_SWEEP: rc = op_ghost_sweep(ctx, l); break;
+    case GMG_OP_SMOOTH: rc = op_smooth(ctx, l, count); break;
+    case GMG_OP_RES_INT: rc = op_res_int(ctx, l, nullptr); break;
+    case GMG_OP_RES_GHOST: rc = op_res_ghost(ctx, l, nullptr); break;
+    case GMG_OP_EXTEND_REXT: rc = op_extend(ctx, l, l.rE); break;
+    case GMG_OP_EXTEND_U: rc = op_extend(ctx, l, l.u); break;
+    case GMG_OP_RESTRICT_INT:
+      if (!has_c) return fail(ctx, "no coarser level");
+      rc = op_restrict_int(ctx, l, ctx->L[li + 1]);
+      break;
+    case GMG_OP_RESTRICT_GHOST:
+      if (!has_c) return fail(ctx, "no coarser level");
+      rc = op_restrict_ghost(ctx, l, ctx->L[li + 1]);
+      break;
+    case GMG_OP_INTERP_ADD:
+      if (!has_c) return fail(ctx, "no coarser level");
+      rc = op_interp(ctx, l, ctx->L[li + 1]);
+      break;
+    case GMG_OP_ZERO_U:
+      GMG_CHECK(ctx, cudaMemsetAsync(l.u, 0, sizeof(double) * l.g.nodes, ctx->stream));
+      break;
+    default: return fail(ctx, "unknown op");
+  }
+  if (rc) return rc;
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  GMG_CHECK(ctx, cudaGetLastError());
+  return 0;
+}
+
+int gmg_cycle(gmg_ctx* ctx, int ncycles) {
+  if (!levels_ready(ctx)) return fail(ctx, "not every level is set");
+  cudaSetDevice(ctx->device);
+  for (int i = 0; i < ncycles; ++i)
+    if (cycle_level(ctx, 0)) return -1;
+  GMG_CHECK(ctx, cudaGetLastError());
+  return 0;
+}
+
+int gmg_residual_norm(gmg_ctx* ctx, int li, double* out) {
+  if (li < 0 || li >= ctx->nlevels || !ctx->L[li].ready) return fail(ctx, "level not set");
+  if (ctx->norm != 0) return fail(ctx, "l2 norm is not available on the device path yet");
+  cudaSetDevice(ctx->device);
+  DevLevel& l = ctx->L[li];
+  GMG_CHECK(ctx, cudaMemsetAsync(ctx->dmax, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  if (op_res_int(ctx, l, ctx->dmax)) return -1;
+  if (op_res_ghost(ctx, l, ctx->dmax + 1)) return -1;
+  GMG_CHECK(ctx, cudaMemcpyAsync(ctx->hmax, ctx->dmax, 2 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  GMG_CHECK(ctx, cudaGetLastError());
+  std::memcpy(out, ctx->hmax, 2 * sizeof(double));
+  return 0;
+}
+
+int gmg_abs_max_scale(gmg_ctx* ctx, double threshold, double factor, double* peak, int* scaled) {
+  cudaSetDevice(ctx->device);
+  DevLevel& l = ctx->L[0];
+  {
+    Scope s(ctx, 7);
+    GMG_CHECK(ctx, cudaMemsetAsync(ctx->dmax + 2, 0, sizeof(unsigned long long), ctx->stream));
+    launch_abs_max(l.u, l.g.nodes, ctx->dmax + 2, ctx->stream);
+    ctx->launches++;
+  }
+  GMG_CHECK(ctx, cudaMemcpyAsync(ctx->hmax + 2, ctx->dmax + 2, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  double p;
+  std::memcpy(&p, ctx->hmax + 2, sizeof(double));
+  *peak = p;
+  *scaled = 0;
+  if (0.0 < p && p < threshold) {
+    launch_scale(l.u, l.g.nodes, factor, ctx->stream);
+    ctx->launches++;
+    *scaled = 1;
+  }
+  GMG_CHECK(ctx, cudaGetLastError());
+  return 0;
+}
+
+int gmg_synchronize(gmg_ctx* ctx) {
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  GMG_CHECK(ctx, cudaGetLastError());
+  return 0;
+}
+
+int64_t gmg_launch_count(const gmg_ctx* ctx) { return ctx->launches; }
+int64_t gmg_device_bytes(const gmg_ctx* ctx) { return ctx->bytes; }
+
+int gmg_profile(gmg_ctx* ctx, int enable) {
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& e : ctx->events) {
+    ctx->pool.push_back(e.a);
+    ctx->pool.push_back(e.b);
+  }
+  ctx->events.clear();
+  ctx->prof = enable != 0;
+  return 0;
+}
+
+int gmg_profile_read(gmg_ctx* ctx, int kclass, double* total_ms, int64_t* count) {
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  double t = 0.0;
+  int64_t n = 0;
+  for (auto& e : ctx->events) {
+    if (e.cls != kclass) continue;
+    float ms = 0.f;
+    GMG_CHECK(ctx, cudaEventElapsedTime(&ms, e.a, e.b));
+    t += ms;
+    n++;
+  }
+  *total_ms = t;
+  *count = n;
+  return 0;
+}
+
+int gmg_uniform_symmetric(uint64_t seed, int64_t n, double* out) {
+  const uint64_t GOLDEN = 0x9E3779B97F4A7C15ull;
+  uint64_t x = seed + GOLDEN;
+  uint64_t z = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  uint64_t s = z ^ (z >> 31);
+  if (s == 0) {
+    x += GOLDEN;
+    z = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    s = z ^ (z >> 31);
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    s ^= s >> 12;
+    s ^= s << 25;
+    s ^= s >> 27;
+    const uint64_t v = s * 2685821657736338717ull;
+    out[i] = 2.0 * ((double)(v >> 11) * 0x1.0p-53) - 1.0;
+  }
+  return 0;
+}
+
+}  // extern "C"

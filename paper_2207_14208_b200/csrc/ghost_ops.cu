@@ -1,0 +1,181 @@
+// ghost_ops.cu -- ghost-row kernels on sm_100a: the batched lexicographic
+// ghost relaxation, the ghost residual and the masked ghost restriction.
+//
+// Ghost data live in "slot" order: ghosts sorted by sweep batch (see
+// transfer.ghost_dag_levels), lexicographic inside a batch.  Weights are
+// stored [m][ng] so a warp reading one stencil entry for 32 ghosts is one
+// coalesced load.
+#include "gmg_kernels.cuh"
+
+namespace gmg {
+
+template <int D>
+__device__ __forceinline__ int64_t block_offset(const Geom& g, int j) {
+  if constexpr (D == 3) {
+    return (int64_t)(j / 9) * g.s0 + (int64_t)((j / 3) % 3) * g.s1 + (j % 3);
+  } else {
+    return (int64_t)(j / 3) * g.s0 + (j % 3);
+  }
+}
+
+// One batch of the ghost sweep (reference smoothing.py:135-142):
+// u_G += dtau * (g - ddot(w, u[block])).  No ghost of a batch reads another
+// ghost of the same batch, so the batch is one parallel step.
+template <int D>
+__global__ void __launch_bounds__(256) ghost_batch_kernel(GhostArgs a, double* __restrict__ u,
+                                                          int64_t lo, int64_t hi) {
+  constexpr int M = D == 3 ? 27 : 9;
+  const int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= hi) return;
+  const int64_t base = a.base[s];
+  double x[M], y[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    x[j] = __ldg(a.w + (int64_t)j * a.ng + s);
+    y[j] = u[base + block_offset<D>(a.g, j)];
+  }
+  const double dot = blas_ddot<M>(x, y);
+  const int64_t node = a.node[s];
+  u[node] = u[node] + a.dtau[s] * (a.gval[s] - dot);
+}
+
+void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st) {
+  if (hi <= lo) return;
+  const int threads = 256;
+  const int64_t blocks = (hi - lo + threads - 1) / threads;
+  if (a.g.d == 3)
+    ghost_batch_kernel<3><<<(unsigned)blocks, threads, 0, st>>>(a, u, lo, hi);
+  else
+    ghost_batch_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(a, u, lo, hi);
+}
+
+__device__ __forceinline__ void block_max_commit(double v, unsigned long long* maxbits) {
+  if (!maxbits) return;
+  __shared__ double part[32];
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) part[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    double x = l < nw ? part[l] : 0.0;
+    x = warp_max(x);
+    if (l == 0) atomic_max_nonneg(maxbits, x);
+  }
+}
+
+// Ghost residual (smoothing.py:120-124): r_g = g - pairwise(w * u[block]),
+// scattered to r_ext at the ghost node; optional max |r_g|.
+template <int D>
+__global__ void __launch_bounds__(256) residual_ghost_kernel(GhostArgs a, const double* __restrict__ u,
+                                                             double* __restrict__ r_ext,
+                                                             unsigned long long* maxbits) {
+  constexpr int M = D == 3 ? 27 : 9;
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double am = 0.0;
+  if (s < a.ng) {
+    const int64_t base = a.base[s];
+    double p[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) p[j] = __ldg(a.w + (int64_t)j * a.ng + s) * u[base + block_offset<D>(a.g, j)];
+    const double r = a.gval[s] - np_sum<M>(p);
+    r_ext[a.node[s]] = r;
+    am = fabs(r);
+  }
+  block_max_commit(am, maxbits);
+}
+
+void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,
+                           unsigned long long* maxbits, cudaStream_t st) {
+  if (a.ng == 0) return;
+  const int threads = 256;
+  const int64_t blocks = (a.ng + threads - 1) / threads;
+  if (a.g.d == 3)
+    residual_ghost_kernel<3><<<(unsigned)blocks, threads, 0, st>>>(a, u, r_ext, maxbits);
+  else
+    residual_ghost_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(a, u, r_ext, maxbits);
+}
+
+// Full-weighting row entry e of a 3^D block, ((1*a)*b)*c.
+template <int D>
+__device__ __forceinline__ double fw_entry(int e) {
+  double v = 1.0;
+  int o[3];
+  int rem = e;
+#pragma unroll
+  for (int k = D - 1; k >= 0; --k) {
+    o[k] = rem % 3;
+    rem /= 3;
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) v = v * (o[k] == 1 ? 0.5 : 0.25);
+  return v;
+}
+
+// GhostRestriction (transfer.py:96-121) for every coarse ghost slot:
+// keep = in-box and (ghost or inactive) on the fine grid, w = FW*keep /
+// pairwise(FW*keep), value = pairwise(w * r_ext[clamped block]); promoted
+// coarse ghosts get 0 (solver.py:189).
+template <int D>
+__global__ void __launch_bounds__(256) restrict_ghost_kernel(Geom gf, const uint8_t* __restrict__ lab_f,
+                                                             const double* __restrict__ r_ext,
+                                                             GhostArgs c, double* __restrict__ gval_c) {
+  constexpr int M = D == 3 ? 27 : 9;
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= c.ng) return;
+  if (c.promoted[s]) {
+    gval_c[s] = 0.0;
+    return;
+  }
+  int64_t node = c.node[s];
+  int64_t mc[3];
+  const int64_t nc = c.g.n;
+#pragma unroll
+  for (int k = D - 1; k >= 0; --k) {
+    mc[k] = node % nc;
+    node /= nc;
+  }
+  const int64_t sf[3] = {gf.s0, gf.s1, gf.s2};
+  double w[M];
+  int64_t blk[M];
+#pragma unroll
+  for (int e = 0; e < M; ++e) {
+    int rem = e, o[3];
+#pragma unroll
+    for (int k = D - 1; k >= 0; --k) {
+      o[k] = rem % 3;
+      rem /= 3;
+    }
+    bool valid = true;
+    int64_t flat = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      int64_t x = 2 * mc[k] + o[k] - 1;
+      if (x < 0 || x > gf.N) valid = false;
+      x = x < 0 ? 0 : (x > gf.N ? gf.N : x);
+      flat += x * sf[k];
+    }
+    blk[e] = flat;
+    const uint8_t L = lab_f[flat];
+    const bool keep = valid && (L == GHOST || L == INACTIVE);
+    w[e] = fw_entry<D>(e) * (keep ? 1.0 : 0.0);
+  }
+  const double sum = np_sum<M>(w);
+  double p[M];
+#pragma unroll
+  for (int e = 0; e < M; ++e) p[e] = (w[e] / sum) * r_ext[blk[e]];
+  gval_c[s] = np_sum<M>(p);
+}
+
+void launch_restrict_ghost(const Geom& gf, const uint8_t* lab_f, const double* r_ext,
+                           const GhostArgs& coarse, double* gval_c, cudaStream_t st) {
+  if (coarse.ng == 0) return;
+  const int threads = 256;
+  const int64_t blocks = (coarse.ng + threads - 1) / threads;
+  if (gf.d == 3)
+    restrict_ghost_kernel<3><<<(unsigned)blocks, threads, 0, st>>>(gf, lab_f, r_ext, coarse, gval_c);
+  else
+    restrict_ghost_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(gf, lab_f, r_ext, coarse, gval_c);
+}
+
+}  // namespace gmg

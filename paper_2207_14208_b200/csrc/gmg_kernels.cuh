@@ -1,0 +1,67 @@
+// gmg_kernels.cuh -- kernel argument blocks and launch entry points.
+#pragma once
+
+#include "gmg_common.cuh"
+
+namespace gmg {
+
+struct GsArgs {
+  Geom g;
+  const uint8_t* labels;
+  double* u;
+  const double* f;
+  const int2* tasks;  // (chunk c, block b) in wavefront order
+  int ntasks;
+  int* ticket;
+  int* progress;      // [C * Bn] completed lines per task
+  int B1, Bn, C;
+};
+
+// Ghost rows of one level, stored in sweep-slot order (batch, then lex).
+struct GhostArgs {
+  Geom g;
+  int64_t ng;
+  const int64_t* node;   // ghost node
+  const int64_t* base;   // flat index of the 3^d block's low corner
+  const double* w;       // [m][ng] row weights, m = 3^d
+  const double* dtau;
+  const double* gval;    // right-hand side per slot
+  const uint8_t* promoted;
+};
+
+struct BandArgs {
+  Geom g;
+  int64_t nb;
+  const int64_t* idx;     // band nodes, BFS groups concatenated
+  const uint8_t* mask;    // BFS assigned-neighbour bits
+  const int8_t* step;     // [nb][d] upwind step
+  const double* absn;     // [nb][d]
+  double* scratch;        // [nb]
+};
+
+void launch_gs_sweep(const GsArgs& a, int grid, cudaStream_t st);
+
+void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st);
+void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,
+                           unsigned long long* maxbits, cudaStream_t st);
+void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,
+                              const double* f, double* r, unsigned long long* maxbits,
+                              cudaStream_t st);
+void launch_band_bfs(const BandArgs& a, double* x, int64_t lo, int64_t hi, cudaStream_t st);
+void launch_band_transport(const BandArgs& a, double* x, cudaStream_t st);
+void launch_restrict_interior(const Geom& gf, const uint8_t* lab_f, const double* r_f,
+                              const Geom& gc, const uint8_t* lab_c, double* f_c,
+                              cudaStream_t st);
+void launch_restrict_ghost(const Geom& gf, const uint8_t* lab_f, const double* r_ext,
+                           const GhostArgs& coarse, double* gval_c, cudaStream_t st);
+void launch_interp_add(const Geom& gf, const uint8_t* lab_f, double* u_f, const Geom& gc,
+                       const double* e_c, cudaStream_t st);
+void launch_abs_max(const double* u, int64_t n, unsigned long long* maxbits, cudaStream_t st);
+void launch_scale(double* u, int64_t n, double s, cudaStream_t st);
+void launch_gather(const int64_t* idx, int64_t n_int, const double* f, const int32_t* ghost_slot,
+                   int64_t n_gh, const double* gval, double* out, cudaStream_t st);
+void launch_scatter(const int64_t* idx, int64_t n, const double* x, double* e, cudaStream_t st);
+void launch_permute(const double* src, const int32_t* perm, int64_t n, double* dst,
+                    cudaStream_t st);
+
+}  // namespace gmg

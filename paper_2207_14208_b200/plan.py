@@ -103,7 +103,9 @@ class LevelPlan:
                 v = int(v)
             elif f.name == "reaction":
                 v = float(v)
-            kw[f.name] = np.asarray(v)
+            else:
+                v = np.asarray(v)
+            kw[f.name] = v
         return cls(**kw)
 
 

@@ -1,0 +1,136 @@
+"""B200 multigrid solver: the reference's solver API over the CUDA library.
+
+Drop-in for /root/reference/pkg/src/ghostmg/solver.py:
+
+* ``build_solver(grid, phi, spec, eliminated_faces, smoother, cycle,
+  default_variant, coarsest_min)`` (solver.py:272-279) builds the hierarchy
+  on the host exactly as the reference does and uploads it once;
+* ``MultigridSolver.solve(u, cycles, tol, seed)`` (solver.py:215-269) and
+  ``measure_rho`` (solver.py:282-298) keep the reference's control flow
+  (``cycle.CycleDriver``) while every cycle runs on the device
+  (``_lib.Context.cycle``), with the iterate resident in HBM between
+  cycles; only the two residual-norm scalars come back per cycle.
+* The coarsest solve is the reference's own: SciPy SuperLU of the assembled
+  coarsest system (solver.py:146-166), called through the library's host
+  callback on a few-KB right-hand side, or ``coarse_solver="sweeps"``
+  (500 device smoothing sweeps).
+"""
+
+import numpy as np
+from scipy.sparse.linalg import splu
+
+from . import _lib
+from .cycle import (
+    NORM_L2,
+    CoarseSolveError,
+    CycleConfig,
+    CycleDriver,
+    CycleReport,
+    measure_rho,
+)
+from .kinds import VARIANT_POLY
+from .plan import coarsest_system
+from .smoothing import SmootherConfig
+from .transfer import build_hierarchy
+
+__all__ = ["MultigridSolver", "build_solver", "measure_rho", "CycleConfig", "CycleReport"]
+
+
+class DeviceHierarchy:
+    """All levels of one solver resident on one GPU."""
+
+    def __init__(self, plans, smoother, cycle, device=0):
+        self.plans = plans
+        d = plans[0].d
+        self.ctx = _lib.Context(d, len(plans), device)
+        for i, p in enumerate(plans):
+            self.ctx.set_level(i, p)
+        coarse_mode = 1 if cycle.coarse_solver == "sweeps" else 0
+        self.ctx.set_cycle(smoother.nu1, smoother.nu2, cycle.gamma, coarse_mode,
+                           cycle.coarse_sweeps, 0)
+        self._lu = None
+        if coarse_mode == 0:
+            self.ctx.set_coarse_callback(self._coarse)
+
+    def _factor(self):
+        if self._lu is None:
+            A, _ = coarsest_system(self.plans[-1])
+            try:
+                self._lu = splu(A.tocsc())
+            except RuntimeError as exc:
+                raise CoarseSolveError(f"coarsest factorization failed: {exc}") from exc
+        return self._lu
+
+    def _coarse(self, rhs):
+        return self._factor().solve(rhs)
+
+
+class MultigridSolver(CycleDriver):
+    """Reference ``MultigridSolver`` with every cycle on the B200."""
+
+    def __init__(self, levels, spec, smoother=None, cycle=None, default_variant=VARIANT_POLY,
+                 device=0):
+        smoother = smoother or SmootherConfig()
+        cycle = cycle or CycleConfig()
+        plans, f, g, e = CycleDriver.problem_data(levels, spec, smoother, default_variant)
+        super().__init__(plans, f, g, e, smoother, cycle)
+        self.levels = levels
+        self.spec = spec
+        self._init_device(device)
+
+    @classmethod
+    def from_plans(cls, plans, f_fine, g_fine, eliminated_values, smoother=None, cycle=None,
+                   device=0):
+        self = cls.__new__(cls)
+        CycleDriver.__init__(self, plans, f_fine, g_fine, eliminated_values,
+                             smoother or SmootherConfig(), cycle or CycleConfig())
+        self.levels = None
+        self.spec = None
+        self._init_device(device)
+        return self
+
+    def _init_device(self, device):
+        if self.cycle_cfg.norm == NORM_L2:
+            raise NotImplementedError("norm='l2' is not implemented on the B200 path yet")
+        self.device = DeviceHierarchy(self.plans, self.smoother, self.cycle_cfg, device)
+        self.ctx = self.device.ctx
+        self._factor_now()
+
+    def _factor_now(self):
+        if self.cycle_cfg.coarse_solver != "sweeps":
+            self.device._factor()
+
+    # ---- primitives --------------------------------------------------------
+    def _set_data(self, f_fine, g_fine):
+        self.ctx.set_vector(0, _lib.F, f_fine)
+        if self.plans[0].n_ghosts:
+            self.ctx.set_vector(0, _lib.G, g_fine)
+
+    def _put_u(self, u):
+        self.ctx.set_vector(0, _lib.U, u)
+
+    def _get_u(self):
+        return self.ctx.get_vector(0, _lib.U, self.plans[0].n_nodes)
+
+    def _run_cycle(self):
+        self.ctx.cycle(1)
+
+    def _residual_norm(self):
+        m_int, m_g = self.ctx.residual_parts(0)
+        p = self.plans[0]
+        m = m_int if p.n_internal else 0.0
+        if p.n_ghosts:
+            m = max(m, m_g)
+        return m
+
+    def _abs_max_scale(self):
+        return self.ctx.abs_max_scale(1e-250, 1e250)
+
+
+def build_solver(grid, phi, spec, eliminated_faces=(), smoother=None, cycle=None,
+                 default_variant=VARIANT_POLY, coarsest_min=4, device=0):
+    """Hierarchy + B200 solver in one call (reference solver.py:272-279)."""
+    cycle = cycle or CycleConfig()
+    levels = build_hierarchy(grid, phi, eliminated_faces, max_levels=cycle.max_levels,
+                             coarsest_min=coarsest_min)
+    return MultigridSolver(levels, spec, smoother, cycle, default_variant, device=device)
