@@ -1,0 +1,339 @@
+"""Benchmark: fine-grid DOF x V-cycles/s (fp64) of the B200 ghost-point
+multigrid V-cycle on BASELINE.json config 4 (3D pore space, 512^3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = one V(2,1) cycle on the finest level plus the residual-norm
+record the reference's ``solve`` makes after every cycle
+(/root/reference/pkg/src/ghostmg/solver.py:224-232).  DOF = internal +
+ghost unknowns of the finest level (the size of the linear system,
+operators.py:180).  Inputs (u, f) are HBM-resident when the timed region
+starts; every array is > L2 (1.08 GB per grid vector at 513^3), so no L2
+flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle
+(oracle/, the C restatement of the reference's per-cycle operators + the
+reference's SciPy SuperLU coarsest solve) on the same workload.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--N", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-cycles", type=int, default=1)
+    return ap.parse_args()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- workload
+def build_workload(args):
+    from paper_2207_14208_b200 import configs as CF
+    from paper_2207_14208_b200.cycle import CycleDriver
+    from paper_2207_14208_b200.transfer import build_hierarchy
+
+    builder = CF.CONFIGS[args.config]
+    setup = builder(args.N) if args.N else builder()
+    t0 = time.time()
+    levels = build_hierarchy(setup.grid, setup.phi, setup.faces, max_levels=setup.cycle.max_levels,
+                             coarsest_min=setup.coarsest_min)
+    t1 = time.time()
+    plans, f, g, e = CycleDriver.problem_data(levels, setup.spec, setup.smoother, setup.default_variant)
+    if setup.f_seed is not None:
+        f = CF.pore_rhs(setup, plans[0].labels)
+    t2 = time.time()
+    log(f"[bench] {setup.name}: hierarchy {t1 - t0:.1f}s, plans {t2 - t1:.1f}s, levels "
+        f"{[p.N for p in plans]}, N_I {plans[0].n_internal}, N_G {plans[0].n_ghosts}")
+    return setup, plans, f, g, e, {"hierarchy_s": round(t1 - t0, 1), "plans_s": round(t2 - t1, 1)}
+
+
+def algorithmic_bytes(plans):
+    """SURVEY.md section 8(d) per-cycle algorithmic bytes (V(2,1)),
+    from the real per-level counts."""
+    total = 0
+    for i, p in enumerate(plans[:-1]):
+        d = p.d
+        m = 3 ** d
+        nI, nG, nB = p.n_internal, p.n_ghosts, p.n_band
+        nIc = plans[i + 1].n_internal
+        sweeps = 3
+        total += sweeps * 24 * nI
+        total += sweeps * nG * (8 * m + 40)
+        total += 16 * nI + 8 * nIc
+        total += nG * (8 * m + 24)
+        total += nB * (8 * (2 * d + 1) + 6 * 8 * (3 * d + 2))
+        total += 16 * (nI + nG) + 8 * nIc
+    p0 = plans[0]
+    total += 16 * p0.n_internal + p0.n_ghosts * (8 * 3 ** p0.d + 24)
+    return total
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the fine-level GS sweep from the committed
+    ncu capture (profiles/ncu_gs_sweep.json), if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_gs_sweep.json")) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- oracle
+def oracle_cycles(plans, f, g, e, setup, cycles, u0=None):
+    """Time `cycles` oracle V-cycles (+ norm) on the host; returns (s, solver)."""
+    from oracle.solver import OracleSolver
+
+    s = OracleSolver(plans, f, g, e, setup.smoother, setup.cycle)
+    s._set_data(f, g)
+    s._put_u(np.zeros(plans[0].n_nodes) if u0 is None else u0)
+    s._coarsest()  # factorization is setup, not per cycle
+    t = time.perf_counter()
+    for _ in range(cycles):
+        s._run_cycle()
+        s._residual_norm()
+    return time.perf_counter() - t, s
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    setup, plans, f, g, e, setup_times = build_workload(args)
+    dof = plans[0].n_internal + plans[0].n_ghosts
+    from oracle.solver import OracleSolver
+
+    s = OracleSolver(plans, f, g, e, setup.smoother, setup.cycle)
+    s._set_data(f, g)
+    s._put_u(np.zeros(plans[0].n_nodes))
+    s._coarsest()
+    for _ in range(args.warmup):
+        s._run_cycle()
+        s._residual_norm()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        s._run_cycle()
+        s._residual_norm()
+    dt = time.perf_counter() - t
+    value = dof * args.steps / dt
+    line = {
+        "impl": "reference", "metric": "fine-grid DOF*V-cycles/s (fp64)", "value": value,
+        "unit": "DOF*cycles/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": setup.name, "N": setup.grid.N, "levels": len(plans), "dof": dof,
+                   "cycle": "V(2,1)", "parallelism": "cpu-1thread"},
+        "cpu_baseline": {"value": value, "unit": "DOF*cycles/s", "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} full V(2,1) cycles at N={setup.grid.N} (C oracle, "
+                                   f"1 thread, SciPy SuperLU coarsest)"},
+        "e2e": {"value": value, "unit": "DOF*cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup": setup_times,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- b200
+def run_b200(args, rank, world, local_rank):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    from paper_2207_14208_b200 import _lib
+    from paper_2207_14208_b200.solver import MultigridSolver
+
+    setup, plans, f, g, e, setup_times = build_workload(args)
+    t0 = time.time()
+    solver = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, device=local_rank)
+    log(f"[bench] upload + coarse factor {time.time() - t0:.1f}s, device bytes "
+        f"{solver.ctx.device_bytes / 1e9:.2f} GB")
+    ctx = solver.ctx
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    p0 = plans[0]
+    dof = p0.n_internal + p0.n_ghosts
+
+    solver._set_data(f, g)
+    solver._put_u(np.zeros(p0.n_nodes))
+    for _ in range(args.warmup):
+        solver._run_cycle()
+        solver._residual_norm()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches0 = ctx.launches
+    ctx.profile(True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            solver._run_cycle()
+            solver._residual_norm()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = ctx.launches - launches0
+    gs_ms, gs_n = ctx.profile_read("gs_sweep", 0)
+    breakdown = {}
+    for k in _lib.KCLASS:
+        tms, n = ctx.profile_read(k)
+        breakdown[k] = round(tms / args.steps, 3)
+    ctx.profile(False)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = dof * args.steps * world / (ms / 1e3)
+
+    # roofline of the dominant kernel (fine-level GS sweep)
+    peak, peak_kind = measured_peak()
+    gs_bytes = 24 * p0.n_internal
+    gs_avg_s = gs_ms / max(gs_n, 1) / 1e3
+    achieved = gs_bytes / gs_avg_s / 1e9 if gs_n else None
+    roofline = {"bound": "hbm", "kernel": "gs_sweep_kernel<3> (finest level)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(),
+                "algorithmic_bytes_per_launch": gs_bytes, "avg_launch_ms": gs_avg_s * 1e3,
+                "launches_timed": gs_n, "peak_source": peak_kind,
+                "cycle_algorithmic_bytes": algorithmic_bytes(plans),
+                "cycle_achieved_gbs": algorithmic_bytes(plans) / (ms / args.steps / 1e3) / 1e9}
+
+    # end to end through the public API: solve() from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        pin_f = torch.empty(p0.n_nodes, dtype=torch.float64, pin_memory=True).numpy()
+        pin_u = torch.empty(p0.n_nodes, dtype=torch.float64, pin_memory=True).numpy()
+        pin_f[:] = f
+        solver.f_fine = pin_f
+        pin_u[:] = 0.0
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        u_out, rep = solver.solve(u=pin_u, cycles=args.steps)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        h2d = 8 * (2 * p0.n_nodes + p0.n_ghosts)
+        d2h = 8 * p0.n_nodes + 16 * (args.steps + 1)
+        e2e = {"value": dof * args.steps * world / dt, "unit": "DOF*cycles/s",
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "solve_s": dt, "cycles": args.steps, "final_residual": rep.residual_norms[-1]}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        n = args.cpu_sample_cycles
+        sec, _ = oracle_cycles(plans, f, g, e, setup, n)
+        cpu = {"value": dof * n / sec, "unit": "DOF*cycles/s", "cores": 1, "kind": "port",
+               "sample": f"{n} V(2,1) cycle(s) + residual norm at N={setup.grid.N} on the host "
+                         f"(C oracle, 1 thread, SciPy SuperLU coarsest), {sec:.1f}s"}
+
+    if rank == 0:
+        line = {
+            "metric": "fine-grid DOF*V-cycles/s (fp64)", "value": value, "unit": "DOF*cycles/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": setup.name, "N": setup.grid.N, "levels": len(plans),
+                       "dof": dof, "N_I": p0.n_internal, "N_G": p0.n_ghosts, "cycle": "V(2,1)",
+                       "coarse": setup.cycle.coarse_solver, "parallelism": f"replicas{world}",
+                       "l2_flush": "not needed: every grid vector (1.08 GB) exceeds L2"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks.summary(), "breakdown_ms_per_cycle": breakdown, "setup": setup_times,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+    else:
+        run_b200(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

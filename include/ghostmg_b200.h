@@ -123,12 +123,14 @@ int64_t gmg_launch_count(const gmg_ctx *ctx);
 /* Device bytes held by the context. */
 int64_t gmg_device_bytes(const gmg_ctx *ctx);
 
-/* Per-kernel-class CUDA-event timing (0 gs sweep, 1 ghost sweep,
- * 2 residuals, 3 band, 4 restriction, 5 interpolation, 6 coarse solve,
- * 7 norms).  gmg_profile(ctx, 1) starts recording, gmg_profile_read
- * synchronizes and returns the summed milliseconds and launch count. */
+/* Per-kernel-class CUDA-event timing on the launch stream (0 gs sweep,
+ * 1 ghost sweep, 2 residuals, 3 band, 4 restriction, 5 interpolation,
+ * 6 coarse solve, 7 norms).  gmg_profile(ctx, 1) clears and starts
+ * recording; gmg_profile_read synchronizes and returns the summed
+ * milliseconds and the number of timed regions of that class on `level`
+ * (-1: all levels). */
 int gmg_profile(gmg_ctx *ctx, int enable);
-int gmg_profile_read(gmg_ctx *ctx, int kclass, double *total_ms, int64_t *count);
+int gmg_profile_read(gmg_ctx *ctx, int kclass, int level, double *total_ms, int64_t *count);
 
 /* Host helper: n draws of the reference's xorshift64* stream from (-1, 1)
  * (ref rng.py:14-56 uniform_symmetric), written to out. */

@@ -48,7 +48,7 @@ SIGNATURES = {
     "gmg_launch_count": (_i64, [_p]),
     "gmg_device_bytes": (_i64, [_p]),
     "gmg_profile": (_i, [_p, _i]),
-    "gmg_profile_read": (_i, [_p, _i, _p, _p]),
+    "gmg_profile_read": (_i, [_p, _i, _i, _p, _p]),
     "gmg_uniform_symmetric": (_i, [ctypes.c_uint64, _i64, _p]),
 }
 
@@ -196,10 +196,10 @@ class Context:
     def profile(self, enable=True):
         self.check(self.lib.gmg_profile(self.ctx, 1 if enable else 0))
 
-    def profile_read(self, kclass):
+    def profile_read(self, kclass, level=-1):
         ms = np.zeros(1)
         cnt = np.zeros(1, dtype=np.int64)
-        self.check(self.lib.gmg_profile_read(self.ctx, KCLASS.get(kclass, kclass), ptr(ms), ptr(cnt)))
+        self.check(self.lib.gmg_profile_read(self.ctx, KCLASS.get(kclass, kclass), level, ptr(ms), ptr(cnt)))
         return float(ms[0]), int(cnt[0])
 
 

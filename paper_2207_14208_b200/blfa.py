@@ -125,3 +125,40 @@ def dtau_opt(query):
     slopes = [abs(g0(query, p)) for p in _corner_ps(max(query.d, 2))]
     x, _ = minimax_lines(slopes)
     return query.h * x if query.bc == BC_NEUMANN else x
+
+
+def dtau_opt_batch(dirichlet, theta, d, h, variant):
+    """``dtau_opt`` for many ghosts at once, bit-identical to the scalar
+    function: the per-corner decay rates are the scalar ones, g0 uses libm
+    ``math.exp`` per element (EXP variant) or exact arithmetic (POLY), and
+    the minimax is 2 / (max + min) in the same order."""
+    import numpy as np
+
+    check_variant(variant)
+    dirichlet = np.asarray(dirichlet, dtype=bool)
+    theta = np.asarray(theta, dtype=float)
+    if np.any((theta < 0.0) | (theta > THETA_FORMULA_MAX)):
+        bad = theta[(theta < 0.0) | (theta > THETA_FORMULA_MAX)][0]
+        raise ValueError(f"theta must lie in [0, {THETA_FORMULA_MAX}], got {bad}")
+    slopes = []
+    for p in _corner_ps(max(d, 2)):
+        if variant == VARIANT_EXP:
+            arg = (-p * theta).tolist()
+            decay = np.fromiter(map(math.exp, arg), dtype=float, count=len(arg))
+            g = np.where(dirichlet, decay, p * decay)
+        else:
+            e = math.exp(-float(p))
+            t = theta
+            dc2, dc1, dc0 = t * (t - 1.0) / 2.0, t * (2.0 - t), (1.0 - t) * (2.0 - t) / 2.0
+            nc2, nc1, nc0 = 0.5 - t, 2.0 * (t - 1.0), 1.5 - t
+            g = np.where(dirichlet, dc0 + dc1 * e + dc2 * e * e, nc0 + nc1 * e + nc2 * e * e)
+        slopes.append(np.abs(g))
+    hi = slopes[0]
+    lo = slopes[0]
+    for s in slopes[1:]:
+        hi = np.maximum(hi, s)
+        lo = np.minimum(lo, s)
+    if np.any(hi == 0.0):
+        raise AllZeroSlopes("all slopes vanish, every x is equally bad")
+    x = 2.0 / (hi + lo)
+    return np.where(dirichlet, x, h * x)

@@ -55,6 +55,7 @@ struct DevLevel {
 struct Prof {
   cudaEvent_t a, b;
   int cls;
+  int level;
 };
 
 }  // namespace
@@ -74,6 +75,7 @@ struct gmg_ctx {
   int64_t launches = 0;
   int64_t bytes = 0;
   bool prof = false;
+  int cur_level = -1;  // level tag for profiling records
   std::vector<Prof> events;
   std::vector<cudaEvent_t> pool;
 };
@@ -117,7 +119,7 @@ int upload(gmg_ctx* ctx, T** p, const T* host, int64_t count) {
 void free_level(DevLevel& l) {
   void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
-                  l.bscratch, l.tasks, l.progress, l.ticket, l.active, l.rhs_d, l.x_d};
+                  l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -149,7 +151,7 @@ struct Scope {
     if (!ctx->prof) return;
     cudaEvent_t b = take();
     cudaEventRecord(b, ctx->stream);
-    ctx->events.push_back({a, b, cls});
+    ctx->events.push_back({a, b, cls, ctx->cur_level});
   }
 };
 
@@ -320,6 +322,7 @@ int coarse_solve(gmg_ctx* ctx, int li) {
 int cycle_level(gmg_ctx* ctx, int li) {
   DevLevel& l = ctx->L[li];
   DevLevel& c = ctx->L[li + 1];
+  ctx->cur_level = li;
   if (op_smooth(ctx, l, ctx->nu1)) return -1;
   if (op_res_int(ctx, l, nullptr)) return -1;
   if (op_res_ghost(ctx, l, nullptr)) return -1;
@@ -327,13 +330,16 @@ int cycle_level(gmg_ctx* ctx, int li) {
   if (op_restrict_int(ctx, l, c)) return -1;
   if (op_restrict_ghost(ctx, l, c)) return -1;
   if (li + 1 == ctx->nlevels - 1) {
+    ctx->cur_level = li + 1;
     if (coarse_solve(ctx, li + 1)) return -1;
   } else {
     GMG_CHECK(ctx, cudaMemsetAsync(c.u, 0, sizeof(double) * (size_t)c.g.nodes, ctx->stream));
     for (int k = 0; k < ctx->gamma; ++k)
       if (cycle_level(ctx, li + 1)) return -1;
   }
+  ctx->cur_level = li + 1;
   if (op_extend(ctx, c, c.u)) return -1;
+  ctx->cur_level = li;
   if (op_interp(ctx, l, c)) return -1;
   return op_smooth(ctx, l, ctx->nu2);
 }
@@ -594,6 +600,7 @@ int gmg_apply(gmg_ctx* ctx, int li, int op, int count) {
   if (li < 0 || li >= ctx->nlevels || !ctx->L[li].ready) return fail(ctx, "level not set");
   cudaSetDevice(ctx->device);
   DevLevel& l = ctx->L[li];
+  ctx->cur_level = li;
   const bool has_c = li + 1 < ctx->nlevels && ctx->L[li + 1].ready;
   int rc = 0;
   switch (op) {
@@ -641,6 +648,7 @@ int gmg_residual_norm(gmg_ctx* ctx, int li, double* out) {
   if (ctx->norm != 0) return fail(ctx, "l2 norm is not available on the device path yet");
   cudaSetDevice(ctx->device);
   DevLevel& l = ctx->L[li];
+  ctx->cur_level = li;
   GMG_CHECK(ctx, cudaMemsetAsync(ctx->dmax, 0, 2 * sizeof(unsigned long long), ctx->stream));
   if (op_res_int(ctx, l, ctx->dmax)) return -1;
   if (op_res_ghost(ctx, l, ctx->dmax + 1)) return -1;
@@ -655,6 +663,7 @@ int gmg_residual_norm(gmg_ctx* ctx, int li, double* out) {
 int gmg_abs_max_scale(gmg_ctx* ctx, double threshold, double factor, double* peak, int* scaled) {
   cudaSetDevice(ctx->device);
   DevLevel& l = ctx->L[0];
+  ctx->cur_level = 0;
   {
     Scope s(ctx, 7);
     GMG_CHECK(ctx, cudaMemsetAsync(ctx->dmax + 2, 0, sizeof(unsigned long long), ctx->stream));
@@ -697,12 +706,12 @@ int gmg_profile(gmg_ctx* ctx, int enable) {
   return 0;
 }
 
-int gmg_profile_read(gmg_ctx* ctx, int kclass, double* total_ms, int64_t* count) {
+int gmg_profile_read(gmg_ctx* ctx, int kclass, int level, double* total_ms, int64_t* count) {
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   double t = 0.0;
   int64_t n = 0;
   for (auto& e : ctx->events) {
-    if (e.cls != kclass) continue;
+    if (e.cls != kclass || (level >= 0 && e.level != level)) continue;
     float ms = 0.f;
     GMG_CHECK(ctx, cudaEventElapsedTime(&ms, e.a, e.b));
     t += ms;

@@ -189,7 +189,7 @@ class PoreSpace(LevelSet):
     gradient of the maximising branch.
     """
 
-    CELLS = 16          # candidate-table resolution per axis
+    CELLS = 40          # candidate-table resolution per axis
     LO, HI = -1.5, 1.5  # candidate-table extent
 
     def __init__(self, centers, radii):
@@ -214,6 +214,11 @@ class PoreSpace(LevelSet):
         lower = (self.radii[None, :] - dmax).max(axis=1)
         self._cand = upper >= lower[:, None] - 1e-6       # (cells, balls)
         self._cell_width = width
+        # CSR of ascending candidate balls per cell
+        self._cand_count = self._cand.sum(axis=1).astype(np.int64)
+        self._cand_ptr = np.zeros(len(self._cand_count) + 1, dtype=np.int64)
+        np.cumsum(self._cand_count, out=self._cand_ptr[1:])
+        self._cand_list = np.nonzero(self._cand)[1].astype(np.int64)
 
     def _cells_of(self, pts):
         m = self.CELLS
@@ -231,25 +236,35 @@ class PoreSpace(LevelSet):
         return self.radii[k] - dist
 
     def _max_and_arg(self, points):
+        """phi and the first maximising ball per point.  Every point is
+        paired with the candidate balls of its cell (all balls outside the
+        table); values of the pairs are reduced per point."""
         pts = np.asarray(points, dtype=float)
         shape = pts.shape[:-1]
         pts = pts.reshape(-1, self.d)
         n = pts.shape[0]
-        best = np.full(n, -np.inf)
-        arg = np.zeros(n, dtype=np.int64)
         if n == 0:
-            return best.reshape(shape), arg.reshape(shape)
+            return np.full(shape, -np.inf), np.zeros(shape, dtype=np.int64)
         cells, outside = self._cells_of(pts)
-        for k in range(len(self.radii)):
-            sel = np.flatnonzero(self._cand[cells, k] | outside)
-            if sel.size == 0:
-                continue
-            v = self._ball_value(pts[sel], k)
-            better = v > best[sel]
-            if np.any(better):
-                w = sel[better]
-                best[w] = v[better]
-                arg[w] = k
+        nball = len(self.radii)
+        counts = self._cand_count[cells]
+        counts[outside] = nball
+        starts = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(counts, out=starts[1:])
+        total = int(starts[-1])
+        owner = np.repeat(np.arange(n), counts)
+        rank = np.arange(total) - starts[owner]
+        cell_of = cells[owner]
+        ball = np.where(outside[owner], rank, self._cand_list[self._cand_ptr[cell_of] + rank])
+        c = self.centers[ball]
+        sq = None
+        for a in range(self.d):
+            t = pts[owner, a] - c[:, a]
+            sq = t * t if sq is None else sq + t * t
+        vals = self.radii[ball] - np.sqrt(sq + 0.0)
+        best = np.maximum.reduceat(vals, starts[:-1])
+        hit = vals == best[owner]
+        arg = np.minimum.reduceat(np.where(hit, ball, nball), starts[:-1])
         return best.reshape(shape), arg.reshape(shape)
 
     def __call__(self, points):

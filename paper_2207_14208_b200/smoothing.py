@@ -57,22 +57,11 @@ def assign_dtau(cls, dirichlet, config, default_variant=VARIANT_POLY):
         dtau = np.where(dirichlet, config.dtau_value, config.dtau_value * h)
     else:
         variant = VARIANT_POLY if config.dtau_mode == DTAU_BLFA_POLY else default_variant
-        theta = cls.ghost_theta_raw
-        dtau = np.empty(ng)
-        # dtau depends on (kind, theta) only; ghosts sharing both share it
-        memo = {}
-        for g in range(ng):
-            if prom[g]:
-                dtau[g] = 1.0
-                continue
-            key = (bool(dirichlet[g]), float(theta[g]))
-            val = memo.get(key)
-            if val is None:
-                val = blfa.dtau_opt(blfa.BlfaQuery(
-                    bc=BC_DIRICHLET if key[0] else BC_NEUMANN, d=cls.grid.d,
-                    theta=key[1], h=h, variant=variant))
-                memo[key] = val
-            dtau[g] = val
+        dtau = np.ones(ng)
+        reg = ~prom
+        if reg.any():
+            dtau[reg] = blfa.dtau_opt_batch(dirichlet[reg], cls.ghost_theta_raw[reg], cls.grid.d, h,
+                                            variant)
     dtau = np.asarray(dtau, dtype=float).copy()
     dtau[prom] = 1.0
     return dtau

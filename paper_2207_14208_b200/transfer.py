@@ -144,12 +144,26 @@ class Level:
     extrap: ExtrapolationPlan
 
 
-def check_transfer(fine_cls, coarse_cls, chunk=1 << 20):
+def check_transfer(fine_cls, coarse_cls, chunk=1 << 20, full_below=1 << 22):
     """Raise what the reference's restriction constructors raise
     (transfer.py:64-114): a coarse internal node whose fine 3^d block leaves
     the box, or whose mixed block holds no internal node; a coarse ghost
-    whose block holds no in-box ghost/inactive node."""
+    whose block holds no in-box ghost/inactive node.
+
+    None of these can fire for nested grids: a coarse internal node is a fine
+    internal node (same point, same phi sign, off the box) at the block
+    centre, and a coarse ghost sits on a fine node with phi >= 0 that is
+    not eliminated (else the coarse node would be too), i.e. a kept
+    ghost/inactive centre.  The exhaustive check runs for grids below
+    ``full_below`` coarse nodes; above that only the block centres are
+    verified."""
     fg, cg = fine_cls.grid, coarse_cls.grid
+    if cg.n_nodes >= full_below:
+        for targets, ok in ((coarse_cls.internal_idx, (INTERNAL,)), (coarse_cls.ghost_idx, (GHOST, INACTIVE))):
+            centers = fg.flat_index(2 * cg.multi_index(targets))
+            if not np.isin(fine_cls.labels[centers], ok).all():
+                raise EmptyStencil("restriction block centre has the wrong label")
+        return
     d = fg.d
     offs = block_offsets(d, 3, -1)
     labels = fine_cls.labels
