@@ -10,6 +10,7 @@
 // coarsest right-hand side when the host SuperLU callback is used.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -44,6 +45,8 @@ struct DevLevel {
   // Gauss-Seidel tasks
   int2* tasks = nullptr;
   int ntasks = 0, B1 = 1, Bn = 1, C = 1;
+  uint32_t* imask = nullptr;  // streaming GS: internal bitmask per (line, chunk)
+  bool stream_gs = false;
   int *progress = nullptr, *ticket = nullptr;
   // coarsest direct solve
   int64_t n_int = 0;
@@ -74,6 +77,8 @@ struct gmg_ctx {
   std::string err;
   int64_t launches = 0;
   int64_t bytes = 0;
+  int sms = 148;
+  bool force_simple_gs = false;
   bool prof = false;
   int cur_level = -1;  // level tag for profiling records
   std::vector<Prof> events;
@@ -119,7 +124,7 @@ int upload(gmg_ctx* ctx, T** p, const T* host, int64_t count) {
 void free_level(DevLevel& l) {
   void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
-                  l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d};  // ticket lives in progress
+                  l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -226,7 +231,11 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
   a.B1 = l.B1;
   a.Bn = l.Bn;
   a.C = l.C;
-  launch_gs_sweep(a, gs_grid(l), ctx->stream);
+  a.imask = l.imask;
+  if (l.stream_gs)
+    launch_gs_stream(a, std::min(l.ntasks, 4 * ctx->sms), 1, ctx->stream);
+  else
+    launch_gs_sweep(a, gs_grid(l), ctx->stream);
   ctx->launches++;
   return 0;
 }
@@ -371,6 +380,8 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
     return nullptr;
   }
   ctx->stream = ctx->own;
+  cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+  if (const char* e = getenv("GMG_SIMPLE_GS")) ctx->force_simple_gs = e[0] == '1';
   if (cudaMalloc(&ctx->dmax, 8 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost(&ctx->hmax, 8 * sizeof(unsigned long long)) != cudaSuccess) {
     delete ctx;
@@ -486,12 +497,25 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
 
   // Gauss-Seidel wavefront tasks
   l.C = (int)((N - 1 + 31) / 32);
+  l.stream_gs = N >= 32 && !ctx->force_simple_gs;
   if (d == 3) {
-    l.B1 = N - 1 >= 512 ? 16 : 8;
+    l.B1 = l.stream_gs ? 16 : 8;
     l.Bn = (int)((N - 1 + l.B1 - 1) / l.B1);
   } else {
     l.B1 = 1;
     l.Bn = 1;
+  }
+  if (l.stream_gs) {
+    // bit j of word (line, c) <=> node k = 1 + 32c + j of that line is internal
+    const int64_t n = N + 1;
+    const int64_t lines = d == 3 ? n * n : n;
+    std::vector<uint32_t> im((size_t)(lines * l.C), 0u);
+    for (int64_t ln = 0; ln < lines; ++ln) {
+      const uint8_t* row = labels + ln * n;
+      for (int64_t k = 1; k <= N - 1; ++k)
+        if (row[k] == INTERNAL) im[(size_t)(ln * l.C + (k - 1) / 32)] |= 1u << ((k - 1) % 32);
+    }
+    if (upload(ctx, &l.imask, im.data(), lines * l.C)) return -1;
   }
   std::vector<int2> tasks;
   for (int s = 0; s <= l.C + l.Bn - 2; ++s)

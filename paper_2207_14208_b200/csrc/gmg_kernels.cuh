@@ -15,6 +15,7 @@ struct GsArgs {
   int* ticket;
   int* progress;      // [C * Bn] completed lines per task
   int B1, Bn, C;
+  const uint32_t* imask;  // per (line, chunk) bitmask of internal nodes (streaming kernel)
 };
 
 // Ghost rows of one level, stored in sweep-slot order (batch, then lex).
@@ -40,6 +41,8 @@ struct BandArgs {
 };
 
 void launch_gs_sweep(const GsArgs& a, int grid, cudaStream_t st);
+void launch_gs_stream(const GsArgs& a, int grid, int warps_per_cta, cudaStream_t st);
+size_t gs_stream_smem_per_warp();
 
 void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st);
 void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,
