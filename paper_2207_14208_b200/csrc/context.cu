@@ -46,7 +46,10 @@ struct DevLevel {
   int2* tasks = nullptr;
   int ntasks = 0, B1 = 1, Bn = 1, C = 1;
   uint32_t* imask = nullptr;  // streaming GS: internal bitmask per (line, chunk)
+  int Cm = 4;                 // imask row stride (C rounded up to 4)
   bool stream_gs = false;
+  bool ws_gs = false;         // warp-specialised TMA kernel
+  WsMaps maps;                // its tensor maps (u, f, imask)
   int *progress = nullptr, *ticket = nullptr;
   // coarsest direct solve
   int64_t n_int = 0;
@@ -79,6 +82,9 @@ struct gmg_ctx {
   int64_t bytes = 0;
   int sms = 148;
   bool force_simple_gs = false;
+  int gs_max_tasks = 0;
+  bool no_ws = false;
+  int ws_ctas_per_sm = 4;
   bool prof = false;
   int cur_level = -1;  // level tag for profiling records
   std::vector<Prof> events;
@@ -166,23 +172,31 @@ Geom make_geom(int d, int64_t N, double reaction) {
   g.d = d;
   g.N = N;
   g.n = N + 1;
+  g.P = ((N + OFF + 1) + 3) / 4 * 4;  // >= n + OFF, multiple of 4 doubles
   if (d == 3) {
-    g.s0 = g.n * g.n;
-    g.s1 = g.n;
+    g.rows = g.n * g.n;
+    g.s0 = g.n * g.P;
+    g.s1 = g.P;
     g.s2 = 1;
-    g.nodes = g.n * g.n * g.n;
   } else {
-    g.s0 = g.n;
+    g.rows = g.n;
+    g.s0 = g.P;
     g.s1 = 1;
     g.s2 = 0;
-    g.nodes = g.n * g.n;
   }
+  g.nodes = g.rows * g.P;
   const double h = 2.0 / (double)N;
   g.h2 = h * h;  // Python h**2 == h*h (correctly rounded square)
   g.denom = 2.0 * d + reaction * g.h2;
   g.inv = 1.0 / g.denom;
   g.c = g.denom / g.h2;
   return g;
+}
+
+// reference flat index (C order over (N+1)^d) -> padded device position
+inline int64_t flat_to_pos(const Geom& g, int64_t flat) {
+  const int64_t row = flat / g.n;
+  return row * g.P + (flat - row * g.n) + OFF;
 }
 
 GhostArgs ghost_args(const DevLevel& l) {
@@ -210,6 +224,35 @@ BandArgs band_args(const DevLevel& l) {
   return a;
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// 2-D tiled tensor map over `rows` rows of `cols` elements (row pitch in bytes)
+bool make_map(CUtensorMap* m, CUtensorMapDataType t, void* base, uint64_t cols, uint64_t rows,
+              uint64_t pitch_bytes, uint32_t box0, uint32_t box1) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_bytes};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, t, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int gs_grid(const DevLevel& l) {
   int warps = std::min(l.ntasks, 148 * 16);
   return std::max(1, (warps + 3) / 4);
@@ -232,7 +275,11 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
   a.Bn = l.Bn;
   a.C = l.C;
   a.imask = l.imask;
-  if (l.stream_gs)
+  a.Cm = l.Cm;
+  if (ctx->gs_max_tasks > 0) a.ntasks = std::min(a.ntasks, ctx->gs_max_tasks);  // timing experiments only
+  if (l.ws_gs)
+    launch_gs_ws(a, l.maps, std::min(a.ntasks, ctx->ws_ctas_per_sm * ctx->sms), ctx->stream);
+  else if (l.stream_gs)
     launch_gs_stream(a, std::min(l.ntasks, 4 * ctx->sms), 1, ctx->stream);
   else
     launch_gs_sweep(a, gs_grid(l), ctx->stream);
@@ -382,6 +429,8 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   ctx->stream = ctx->own;
   cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* e = getenv("GMG_SIMPLE_GS")) ctx->force_simple_gs = e[0] == '1';
+  if (const char* e = getenv("GMG_GS_MAX_TASKS")) ctx->gs_max_tasks = atoi(e);
+  if (const char* e = getenv("GMG_NO_WS")) ctx->no_ws = e[0] == '1';
   if (cudaMalloc(&ctx->dmax, 8 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost(&ctx->hmax, 8 * sizeof(unsigned long long)) != cudaSuccess) {
     delete ctx;
@@ -429,15 +478,24 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   l.N = N;
   l.g = make_geom(d, N, reaction);
   const int64_t nodes = l.g.nodes;
+  const int64_t nflat = l.g.rows * l.g.n;
   const int m = d == 3 ? 27 : 9;
-  if (upload(ctx, &l.labels, labels, nodes)) return -1;
-  if (dalloc(ctx, &l.u, nodes) || dalloc(ctx, &l.f, nodes) || dalloc(ctx, &l.rI, nodes) ||
-      dalloc(ctx, &l.rE, nodes))
+  {
+    std::vector<uint8_t> lab((size_t)nodes, (uint8_t)PAD);
+    for (int64_t r = 0; r < l.g.rows; ++r)
+      std::memcpy(&lab[(size_t)(r * l.g.P + OFF)], labels + r * l.g.n, (size_t)l.g.n);
+    if (upload(ctx, &l.labels, lab.data(), nodes)) return -1;
+  }
+  // grid vectors carry two spare rows so row-segment loads near the end
+  // of the array stay inside the allocation
+  const int64_t alloc = nodes + 2 * l.g.P;
+  if (dalloc(ctx, &l.u, alloc) || dalloc(ctx, &l.f, alloc) || dalloc(ctx, &l.rI, alloc) ||
+      dalloc(ctx, &l.rE, alloc))
     return -1;
-  GMG_CHECK(ctx, cudaMemset(l.u, 0, sizeof(double) * nodes));
-  GMG_CHECK(ctx, cudaMemset(l.f, 0, sizeof(double) * nodes));
-  GMG_CHECK(ctx, cudaMemset(l.rI, 0, sizeof(double) * nodes));
-  GMG_CHECK(ctx, cudaMemset(l.rE, 0, sizeof(double) * nodes));
+  GMG_CHECK(ctx, cudaMemset(l.u, 0, sizeof(double) * alloc));
+  GMG_CHECK(ctx, cudaMemset(l.f, 0, sizeof(double) * alloc));
+  GMG_CHECK(ctx, cudaMemset(l.rI, 0, sizeof(double) * alloc));
+  GMG_CHECK(ctx, cudaMemset(l.rE, 0, sizeof(double) * alloc));
 
   // ghosts -> slot order (stable by batch)
   l.ng = ng;
@@ -461,8 +519,8 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     const int64_t st[3] = {l.g.s0, l.g.s1, l.g.s2};
     for (int64_t s = 0; s < ng; ++s) {
       const int64_t i = s2l[s];
-      node[s] = ghost_idx[i];
-      int64_t b = 0;
+      node[s] = flat_to_pos(l.g, ghost_idx[i]);
+      int64_t b = OFF;
       for (int k = 0; k < d; ++k) b += ghost_low[i * d + k] * st[k];
       base[s] = b;
       for (int j = 0; j < m; ++j) w[(size_t)j * ng + s] = ghost_w[i * m + j];
@@ -489,7 +547,9 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   }
   l.nb = nb;
   if (nb > 0) {
-    if (upload(ctx, &l.band_idx, band_idx, nb) || upload(ctx, &l.bfs_mask, bfs_mask, nb) ||
+    std::vector<int64_t> bpos((size_t)nb);
+    for (int64_t q = 0; q < nb; ++q) bpos[q] = flat_to_pos(l.g, band_idx[q]);
+    if (upload(ctx, &l.band_idx, bpos.data(), nb) || upload(ctx, &l.bfs_mask, bfs_mask, nb) ||
         upload(ctx, &l.tstep, trans_step, nb * d) || upload(ctx, &l.tabsn, trans_absn, nb * d) ||
         dalloc(ctx, &l.bscratch, nb))
       return -1;
@@ -498,6 +558,7 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   // Gauss-Seidel wavefront tasks
   l.C = (int)((N - 1 + 31) / 32);
   l.stream_gs = N >= 32 && !ctx->force_simple_gs;
+  l.ws_gs = N >= 64 && !ctx->force_simple_gs && !ctx->no_ws && encode_fn() != nullptr;
   if (d == 3) {
     l.B1 = l.stream_gs ? 16 : 8;
     l.Bn = (int)((N - 1 + l.B1 - 1) / l.B1);
@@ -509,13 +570,22 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     // bit j of word (line, c) <=> node k = 1 + 32c + j of that line is internal
     const int64_t n = N + 1;
     const int64_t lines = d == 3 ? n * n : n;
-    std::vector<uint32_t> im((size_t)(lines * l.C), 0u);
+    l.Cm = (l.C + 3) / 4 * 4;
+    std::vector<uint32_t> im((size_t)(lines * l.Cm), 0u);
     for (int64_t ln = 0; ln < lines; ++ln) {
       const uint8_t* row = labels + ln * n;
       for (int64_t k = 1; k <= N - 1; ++k)
-        if (row[k] == INTERNAL) im[(size_t)(ln * l.C + (k - 1) / 32)] |= 1u << ((k - 1) % 32);
+        if (row[k] == INTERNAL) im[(size_t)(ln * l.Cm + (k - 1) / 32)] |= 1u << ((k - 1) % 32);
     }
-    if (upload(ctx, &l.imask, im.data(), lines * l.C)) return -1;
+    if (upload(ctx, &l.imask, im.data(), lines * l.Cm)) return -1;
+    if (l.ws_gs) {
+      const uint64_t P = (uint64_t)l.g.P;
+      if (!make_map(&l.maps.u, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, l.u, P, (uint64_t)l.g.rows, P * 8, 36, 8) ||
+          !make_map(&l.maps.f, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, l.f, P, (uint64_t)l.g.rows, P * 8, 32, 8) ||
+          !make_map(&l.maps.m, CU_TENSOR_MAP_DATA_TYPE_UINT32, l.imask, (uint64_t)l.Cm, (uint64_t)lines,
+                    (uint64_t)l.Cm * 4, 4, 8))
+        return fail(ctx, "cuTensorMapEncodeTiled failed");
+    }
   }
   std::vector<int2> tasks;
   for (int s = 0; s <= l.C + l.Bn - 2; ++s)
@@ -531,10 +601,10 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   // coarsest direct-solve ordering: internal then ghost (ref operators.py:180)
   if (li == ctx->nlevels - 1) {
     std::vector<int64_t> act;
-    for (int64_t i = 0; i < nodes; ++i)
-      if (labels[i] == INTERNAL) act.push_back(i);
+    for (int64_t i = 0; i < nflat; ++i)
+      if (labels[i] == INTERNAL) act.push_back(flat_to_pos(l.g, i));
     l.n_int = (int64_t)act.size();
-    for (int64_t i = 0; i < ng; ++i) act.push_back(ghost_idx[i]);
+    for (int64_t i = 0; i < ng; ++i) act.push_back(flat_to_pos(l.g, ghost_idx[i]));
     const int64_t n = (int64_t)act.size();
     if (upload(ctx, &l.active, act.data(), n) || dalloc(ctx, &l.rhs_d, n) || dalloc(ctx, &l.x_d, n))
       return -1;
@@ -591,7 +661,8 @@ int gmg_set_vector(gmg_ctx* ctx, int li, int which, const double* host) {
   }
   double* p = vec_ptr(l, which);
   if (!p) return fail(ctx, "unknown vector");
-  GMG_CHECK(ctx, cudaMemcpyAsync(p, host, sizeof(double) * l.g.nodes, cudaMemcpyHostToDevice, ctx->stream));
+  GMG_CHECK(ctx, cudaMemcpy2DAsync(p + OFF, sizeof(double) * l.g.P, host, sizeof(double) * l.g.n,
+                                   sizeof(double) * l.g.n, l.g.rows, cudaMemcpyHostToDevice, ctx->stream));
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   return 0;
 }
@@ -610,7 +681,8 @@ int gmg_get_vector(gmg_ctx* ctx, int li, int which, double* host) {
   }
   double* p = vec_ptr(l, which);
   if (!p) return fail(ctx, "unknown vector");
-  GMG_CHECK(ctx, cudaMemcpyAsync(host, p, sizeof(double) * l.g.nodes, cudaMemcpyDeviceToHost, ctx->stream));
+  GMG_CHECK(ctx, cudaMemcpy2DAsync(host, sizeof(double) * l.g.n, p + OFF, sizeof(double) * l.g.P,
+                                   sizeof(double) * l.g.n, l.g.rows, cudaMemcpyDeviceToHost, ctx->stream));
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   return 0;
 }

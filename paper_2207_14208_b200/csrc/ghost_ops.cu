@@ -127,15 +127,8 @@ __global__ void __launch_bounds__(256) restrict_ghost_kernel(Geom gf, const uint
     gval_c[s] = 0.0;
     return;
   }
-  int64_t node = c.node[s];
   int64_t mc[3];
-  const int64_t nc = c.g.n;
-#pragma unroll
-  for (int k = D - 1; k >= 0; --k) {
-    mc[k] = node % nc;
-    node /= nc;
-  }
-  const int64_t sf[3] = {gf.s0, gf.s1, gf.s2};
+  pos_multi(c.g, c.node[s], mc);
   double w[M];
   int64_t blk[M];
 #pragma unroll
@@ -147,14 +140,14 @@ __global__ void __launch_bounds__(256) restrict_ghost_kernel(Geom gf, const uint
       rem /= 3;
     }
     bool valid = true;
-    int64_t flat = 0;
+    int64_t mf[3];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       int64_t x = 2 * mc[k] + o[k] - 1;
       if (x < 0 || x > gf.N) valid = false;
-      x = x < 0 ? 0 : (x > gf.N ? gf.N : x);
-      flat += x * sf[k];
+      mf[k] = x < 0 ? 0 : (x > gf.N ? gf.N : x);
     }
+    const int64_t flat = multi_pos(gf, mf);
     blk[e] = flat;
     const uint8_t L = lab_f[flat];
     const bool keep = valid && (L == GHOST || L == INACTIVE);

@@ -13,7 +13,7 @@
 
 namespace gmg {
 
-enum Label : uint8_t { INTERNAL = 0, GHOST = 1, INACTIVE = 2, ELIMINATED = 3 };
+enum Label : uint8_t { INTERNAL = 0, GHOST = 1, INACTIVE = 2, ELIMINATED = 3, PAD = 4 };
 
 // Left-to-right sum of n < 8 terms, then + 0.0: NumPy's add.reduce over a
 // short axis (an all-zero result comes out as +0).
@@ -89,13 +89,42 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// Device grid layout: rows along the fastest axis are padded to a pitch P
+// (multiple of 4 doubles, >= N + 4) and node k of a row sits at column
+// k + OFF with OFF = 3, so column k0 = 1 + 32c of every row is 32-byte
+// aligned.  pos(i0, i1, k) = (i0 * n + i1) * P + k + OFF in 3-D,
+// i0 * P + k + OFF in 2-D.  Padding columns carry label PAD and value 0.
+constexpr int64_t OFF = 3;
+
 struct Geom {
-  int d;           // 2 or 3 (1 is mapped to a 2-D layout with one line)
-  int64_t N;       // cells per axis
-  int64_t n;       // N + 1 nodes per axis
-  int64_t s0, s1, s2;  // flat strides of axes 0, 1, 2 (s2 = 1 in 3-D)
-  int64_t nodes;
+  int d;               // 2 or 3
+  int64_t N;           // cells per axis
+  int64_t n;           // N + 1 nodes per axis
+  int64_t P;           // row pitch (doubles)
+  int64_t rows;        // n^2 (3-D) or n (2-D)
+  int64_t s0, s1, s2;  // position strides of axes 0, 1, 2 (the fastest axis has stride 1)
+  int64_t nodes;       // allocated positions = rows * P
   double h2, denom, inv, c;  // h^2, 2d + reaction h^2, 1/denom, denom/h^2
 };
+
+// position -> multi-index (m[d-1] is the fastest axis); returns false on padding
+__device__ __forceinline__ bool pos_multi(const Geom& g, int64_t pos, int64_t* m) {
+  const int64_t row = pos / g.P;
+  const int64_t k = pos - row * g.P - OFF;
+  if (g.d == 3) {
+    m[0] = row / g.n;
+    m[1] = row - m[0] * g.n;
+    m[2] = k;
+  } else {
+    m[0] = row;
+    m[1] = k;
+  }
+  return k >= 0 && k <= g.N;
+}
+
+__device__ __forceinline__ int64_t multi_pos(const Geom& g, const int64_t* m) {
+  if (g.d == 3) return (m[0] * g.n + m[1]) * g.P + m[2] + OFF;
+  return m[0] * g.P + m[1] + OFF;
+}
 
 }  // namespace gmg

@@ -1,6 +1,8 @@
 // gmg_kernels.cuh -- kernel argument blocks and launch entry points.
 #pragma once
 
+#include <cuda.h>
+
 #include "gmg_common.cuh"
 
 namespace gmg {
@@ -15,7 +17,8 @@ struct GsArgs {
   int* ticket;
   int* progress;      // [C * Bn] completed lines per task
   int B1, Bn, C;
-  const uint32_t* imask;  // per (line, chunk) bitmask of internal nodes (streaming kernel)
+  const uint32_t* imask;  // per (line, chunk) bitmask of internal nodes, row stride Cm
+  int Cm;                 // C rounded up to a multiple of 4
 };
 
 // Ghost rows of one level, stored in sweep-slot order (batch, then lex).
@@ -43,6 +46,12 @@ struct BandArgs {
 void launch_gs_sweep(const GsArgs& a, int grid, cudaStream_t st);
 void launch_gs_stream(const GsArgs& a, int grid, int warps_per_cta, cudaStream_t st);
 size_t gs_stream_smem_per_warp();
+// TMA tensor maps of one level for the warp-specialised GS kernel
+struct WsMaps {
+  CUtensorMap u, f, m;
+};
+void launch_gs_ws(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st);
+size_t gs_ws_smem();
 
 void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st);
 void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,

@@ -97,16 +97,11 @@ __global__ void __launch_bounds__(256) restrict_interior_kernel(Geom gf, const u
   for (int64_t ic = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ic < gc.nodes;
        ic += (int64_t)gridDim.x * blockDim.x) {
     if (lab_c[ic] != INTERNAL) continue;
-    int64_t rem = ic, mc[3];
+    int64_t mc[3];
+    pos_multi(gc, ic, mc);
 #pragma unroll
-    for (int k = D - 1; k >= 0; --k) {
-      mc[k] = rem % gc.n;
-      rem /= gc.n;
-    }
-    int64_t center = 0;
-    const int64_t sf[3] = {gf.s0, gf.s1, gf.s2};
-#pragma unroll
-    for (int k = 0; k < D; ++k) center += 2 * mc[k] * sf[k];
+    for (int k = 0; k < D; ++k) mc[k] *= 2;
+    const int64_t center = multi_pos(gf, mc);
     int64_t blk[M];
     bool mixed = false;
     int cnt = 0;
@@ -162,23 +157,22 @@ __global__ void __launch_bounds__(256) interp_add_kernel(Geom gf, const uint8_t*
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint8_t L = lab_f[i];
     if (L != INTERNAL && L != GHOST) continue;
-    int64_t rem = i, m[3];
+    int64_t m[3], half[3];
+    pos_multi(gf, i, m);
 #pragma unroll
-    for (int k = D - 1; k >= 0; --k) {
-      m[k] = rem % gf.n;
-      rem /= gf.n;
-    }
+    for (int k = 0; k < D; ++k) half[k] = m[k] / 2;
+    const int64_t cbase = multi_pos(gc, half);
     double p[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       double w = 1.0;
-      int64_t src = 0;
+      int64_t src = cbase;
 #pragma unroll
       for (int k = 0; k < D; ++k) {
         const int off = (c >> (D - 1 - k)) & 1;
         const int odd = (int)(m[k] & 1);
         w = w * (odd ? 0.5 : (off == 0 ? 1.0 : 0.0));
-        src += (m[k] / 2 + (odd ? off : 0)) * sc[k];
+        src += (odd ? off : 0) * sc[k];
       }
       p[c] = w * e[src];
     }

@@ -19,6 +19,8 @@
 //    coalesced 256-byte row.
 //
 // Reference: gs_lex_sweep, /root/reference/pkg/src/ghostmg/smoothing.py:127-132.
+#include <cstddef>
+
 #include "gmg_kernels.cuh"
 
 namespace gmg {
@@ -30,28 +32,35 @@ constexpr int RLF = 64;   // f ring lines
 constexpr int RP = 8;     // plane-row ring (3-D)
 constexpr int PFU = 64;   // u prefetch distance (lines)
 constexpr int PFF = 32;   // f / halo prefetch distance (lines)
+// u ring row: [0] k0-2, [1] k0-1 (new left halo from chunk c-1), [2..33]
+// columns k0..k0+31, [34] k0+32 (old right halo), [35] k0+33.  With the
+// padded device layout every 16-byte chunk of that range is aligned, and the
+// pitch of 36 doubles keeps the skewed diagonal access (lane j on row t-j)
+// free of bank conflicts.
+constexpr int UP = 36;
 
 struct __align__(16) WarpRing {
-  double u[RLU][32];
+  double u[RLU][UP];
   double f[RLF][32];
-  double up[RP][34];  // row above the block (16-B aligned superset), new values
-  double dn[RP][32];  // row below the block, old values
-  double hr[RLU];     // old right halo k0+32
-  double hl[RLF][2];  // new left halo k0-1 (16-B aligned pair)
+  double up[RP][32];  // row above the block (new values), 3-D
+  double dn[RP][32];  // row below the block (old values), 3-D
   uint32_t mask[RLF];
 };
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cp8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void cp16p(unsigned dst, const void* src, bool p) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q cp.async.ca.shared.global [%0], [%1], 16;\n}\n"
+               ::"r"(dst), "l"(src), "r"((int)p));
 }
-__device__ __forceinline__ void cp4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void cp16cgp(unsigned dst, const void* src, bool p) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q cp.async.cg.shared.global [%0], [%1], 16;\n}\n"
+               ::"r"(dst), "l"(src), "r"((int)p));
 }
-__device__ __forceinline__ void cp16cg(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void cp4p(unsigned dst, const void* src, bool p) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q cp.async.ca.shared.global [%0], [%1], 4;\n}\n"
+               ::"r"(dst), "l"(src), "r"((int)p));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -67,26 +76,34 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// line L of a task -> (plane p, row r), for L >= -R (p = -1 is the boundary
-// plane i0 = 0, p = P the boundary plane i0 = N).
-struct LinePos {
-  int p, r;
-  __device__ void init(int L, int R) {
-    p = L >= 0 ? L / R : -((-L + R - 1) / R);  // floor(L / R)
-    r = L - p * R;
+// Uniform line stream of a task: line L, row r, plane p, device position of
+// (line, column k0) and index of the line's internal-bitmask word.
+struct Stream {
+  int L, r, p;
+  int64_t off;
+  int64_t mw;
+  __device__ __forceinline__ void init(int L0, int R, int64_t pos0, int64_t s0, int64_t s1,
+                                       int64_t mw0, int64_t mplane, int64_t mrow) {
+    L = L0;
+    p = L0 >= 0 ? L0 / R : -((-L0 + R - 1) / R);  // floor(L0 / R)
+    r = L0 - p * R;
+    off = pos0 + (int64_t)(p + 1) * s0 + (int64_t)r * s1;
+    mw = mw0 + (int64_t)(p + 1) * mplane + (int64_t)r * mrow;
   }
-  __device__ void next(int R) {
-    if (++r == R) {
-      r = 0;
-      ++p;
-    }
+  __device__ __forceinline__ void next(int R, int64_t s1, int64_t wrap, int64_t mrow, int64_t mwrap) {
+    ++L;
+    const bool w = ++r == R;
+    r = w ? 0 : r;
+    p += w;
+    off += w ? wrap : s1;
+    mw += w ? mwrap : mrow;
   }
 };
 
 }  // namespace
 
 template <int DIM>
-__global__ void __launch_bounds__(128, 1) gs_stream_kernel(GsArgs a) {
+__global__ void __launch_bounds__(32) gs_stream_kernel(GsArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -95,138 +112,135 @@ __global__ void __launch_bounds__(128, 1) gs_stream_kernel(GsArgs a) {
   const int N = (int)g.N;
   double* __restrict__ u = a.u;
   const double* __restrict__ f = a.f;
+  const double h2 = g.h2, inv = g.inv;
+  const unsigned sbase = smem_addr(&S);
+  const unsigned sU16 = sbase + (unsigned)offsetof(WarpRing, u) + 16u + 16u * lane;  // row[2 + 2 lane]
+  const unsigned sU0 = sbase + (unsigned)offsetof(WarpRing, u);
+  const unsigned sF16 = sbase + (unsigned)offsetof(WarpRing, f) + 16u * lane;
+  const unsigned sUP16 = sbase + (unsigned)offsetof(WarpRing, up) + 16u * lane;
+  const unsigned sDN16 = sbase + (unsigned)offsetof(WarpRing, dn) + 16u * lane;
+  const unsigned sM = sbase + (unsigned)offsetof(WarpRing, mask);
+  const bool lane0 = lane == 0;
+  const bool l16 = lane < 16;
+  const bool l17 = lane < 17;
 
   for (;;) {
     int tid = 0;
-    if (lane == 0) tid = atomicAdd(a.ticket, 1);
+    if (lane0) tid = atomicAdd(a.ticket, 1);
     tid = __shfl_sync(FULL, tid, 0);
     if (tid >= a.ntasks) return;
     const int2 tk = a.tasks[tid];
     const int c = tk.x, b = tk.y;
     const int k0 = 1 + 32 * c;
-    const int k = k0 + lane;
-    const bool kval = k <= N - 1;
+    const bool kval = k0 + lane <= N - 1;  // interior column
     const int R = DIM == 3 ? min(a.B1, N - 1 - b * a.B1) : 1;
     const int nLines = (N - 1) * R;
-    const int uEnd = nLines + R;  // u lines run over [-R, nLines + R)
+    const int uEnd = nLines + R;
     const int rowbase = DIM == 3 ? 1 + b * a.B1 : 0;
+    const int64_t s0 = g.s0;
+    const int64_t s1 = DIM == 3 ? g.s1 : g.s0;  // next row (3-D) / next line (2-D)
+    const int64_t wrap = DIM == 3 ? g.s0 - (int64_t)(R - 1) * g.s1 : g.s0;
+    const int64_t pos0 = (DIM == 3 ? (int64_t)rowbase * g.s1 : 0) + k0 + OFF;  // plane i0 = 0
+    const int64_t mplane = DIM == 3 ? (int64_t)g.n * a.Cm : (int64_t)a.Cm;
+    const int64_t mrow = DIM == 3 ? (int64_t)a.Cm : mplane;
+    const int64_t mwrap = DIM == 3 ? mplane - (int64_t)(R - 1) * a.Cm : mplane;
+    const int64_t mw0 = (DIM == 3 ? (int64_t)rowbase * a.Cm : 0) + c;  // mask word of plane i0 = 0
     int* myprog = a.progress + c * a.Bn + b;
     const int* lprog = c > 0 ? a.progress + (c - 1) * a.Bn + b : nullptr;
     const int* uprog = (DIM == 3 && b > 0) ? a.progress + c * a.Bn + (b - 1) : nullptr;
     int seenL = 0, seenU = 0;
 
-    auto line_node = [&](int p, int r) -> int64_t {
-      if (DIM == 3) return (int64_t)(p + 1) * g.s0 + (int64_t)(rowbase + r) * g.s1 + k0;
-      return (int64_t)(p + 1) * g.s0 + k0;
-    };
-    auto line_mask = [&](int p, int r) -> int64_t {
-      if (DIM == 3) return ((int64_t)(p + 1) * g.n + rowbase + r) * a.C + c;
-      return (int64_t)(p + 1) * a.C + c;
-    };
-
     const int t0 = -(PFU + R);
-    LinePos pu, pf, pc;   // prefetch-u, prefetch-f, compute (this lane's line)
-    pu.init(t0 + PFU, R);
-    pf.init(t0 + PFF, R);
-    pc.init(t0 - lane, R);
-    double mine = 0.0, prev = 0.0;
+    Stream pu, pf, pd;
+    pu.init(t0 + PFU, R, pos0, s0, s1, mw0, mplane, mrow);
+    pf.init(t0 + PFF, R, pos0, s0, s1, mw0, mplane, mrow);
+    pd.init(t0 - 31, R, pos0, s0, s1, mw0, mplane, mrow);
+    // this lane's compute line nl = t - lane: row within the plane and plane slot
+    int cr, cp;
+    {
+      const int L0 = t0 - lane;
+      cp = L0 >= 0 ? L0 / R : -((-L0 + R - 1) / R);
+      cr = L0 - cp * R;
+    }
+    double prev = 0.0;
     const int last = nLines + 30;
 
     for (int t = t0; t <= last; ++t) {
-      // ---------------- prefetch (one commit group per step) --------------
-      const int Lu = t + PFU;
-      if (Lu >= -R && Lu < uEnd) {
-        const int64_t n0 = line_node(pu.p, pu.r);
-        const int su = Lu & (RLU - 1);
-        if (k0 + lane <= N) cp8(&S.u[su][lane], u + n0 + lane);
-        if (lane == 0 && k0 + 32 <= N) cp8(&S.hr[su], u + n0 + 32);
+      // ---------------- prefetch: one cp.async group per step -------------
+      if (pu.L < uEnd) {
+        const unsigned row = sU16 + (unsigned)(pu.L & (RLU - 1)) * (8u * UP);
+        cp16p(row, u + pu.off + 2 * lane, l17);
       }
-      const int Lf = t + PFF;
-      if (Lf >= 0 && Lf < nLines) {
-        const int64_t n0 = line_node(pf.p, pf.r);
-        const int sf = Lf & (RLF - 1);
-        if (k0 + lane <= N - 1) cp8(&S.f[sf][lane], f + n0 + lane);
-        if (lane == 0) {
-          cp4(&S.mask[sf], a.imask + line_mask(pf.p, pf.r));
-          if (lprog)
-            while (seenL < Lf + 1) seenL = ld_acquire(lprog);
-          if (DIM == 3 && uprog && pf.r == 0) {
-            const int need = (pf.p + 1) * a.B1;
-            while (seenU < need) seenU = ld_acquire(uprog);
-          }
+      pu.next(R, s1, wrap, mrow, mwrap);
+      if (pf.L >= 0 && pf.L < nLines) {
+        const unsigned sf = (unsigned)(pf.L & (RLF - 1));
+        cp16p(sF16 + sf * 256u, f + pf.off + 2 * lane, l16);
+        cp4p(sM + sf * 4u, a.imask + pf.mw, lane0);
+        const bool plane_start = DIM == 3 && pf.r == 0;
+        // producers' progress: every lane polls the same word (no divergence)
+        if (lprog)
+          while (seenL < pf.L + 1) seenL = ld_acquire(lprog);
+        if (uprog && plane_start) {
+          const int need = (pf.p + 1) * a.B1;
+          while (seenU < need) seenU = ld_acquire(uprog);
         }
-        __syncwarp();
-        if (lane == 0) cp16cg(&S.hl[sf][0], u + ((n0 - 1) & ~(int64_t)1));
-        if (DIM == 3 && pf.r == 0) {
-          const int sp = pf.p & (RP - 1);
-          const int64_t up0 = n0 - g.s1;  // row rowbase - 1, column k0
-          const int64_t upa = up0 & ~(int64_t)1;
-          if (lane < 17) cp16cg(&S.up[sp][2 * lane], u + upa + 2 * lane);
-          const int64_t dn0 = n0 + (int64_t)R * g.s1;  // row rowbase + R
-          if (k0 + lane <= N) cp8(&S.dn[sp][lane], u + dn0 + lane);
+        cp16cgp(sU0 + (unsigned)(pf.L & (RLU - 1)) * (8u * UP), u + pf.off - 2, lane0);
+        if (plane_start) {
+          const unsigned sp = (unsigned)(pf.p & (RP - 1)) * 256u;
+          cp16cgp(sUP16 + sp, u + pf.off - g.s1 + 2 * lane, l16);
+          cp16p(sDN16 + sp, u + pf.off + (int64_t)R * g.s1 + 2 * lane, l16);
         }
       }
+      pf.next(R, s1, wrap, mrow, mwrap);
       cp_commit();
-      pu.next(R);
-      pf.next(R);
       cp_wait<PFF>();
       __syncwarp();
 
-      // ---------------- compute: lane j on line t - j ----------------------
-      const int nl = t - lane;
-      const double left = __shfl_up_sync(FULL, mine, 1);
-      if (nl >= 0 && nl < nLines && kval) {
+      // ---------------- compute: lane j on line t - j (branch-free) --------
+      {
+        const int nl = t - lane;
+        const bool valid = kval && nl >= 0 && nl < nLines;
         const int su = nl & (RLU - 1);
         const int sf = nl & (RLF - 1);
-        const double old = S.u[su][lane];
-        if ((S.mask[sf] >> lane) & 1u) {
-          const double fv = S.f[sf][lane];
-          const double a0m = S.u[(nl - R) & (RLU - 1)][lane];
-          const double a0p = S.u[(nl + R) & (RLU - 1)][lane];
-          double kp = lane < 31 ? S.u[su][lane + 1] : S.hr[su];
-          double km = left;
-          if (lane == 0) {
-            const int64_t e = line_node(pc.p, pc.r) - 1;
-            km = S.hl[sf][(int)(e & 1)];
-          }
-          double s;
-          if (DIM == 3) {
-            double rm, rp;
-            const int sp = pc.p & (RP - 1);
-            if (pc.r > 0) {
-              rm = prev;
-            } else {
-              const int64_t up0 = line_node(pc.p, 0) - g.s1;
-              rm = S.up[sp][(int)(up0 & 1) + lane];
-            }
-            rp = pc.r < R - 1 ? S.u[(nl + 1) & (RLU - 1)][lane] : S.dn[sp][lane];
-            s = ((((a0m + a0p) + rm) + rp) + km) + kp;
-          } else {
-            s = ((a0m + a0p) + km) + kp;
-          }
-          s = s + 0.0;
-          mine = (g.h2 * fv + s) * g.inv;
-          S.u[su][lane] = mine;
+        const double* row = S.u[su];
+        const double hf = h2 * S.f[sf][lane] + 0.0;  // (h2 f + 0) + S == h2 f + (S + 0)
+        const double a0m = S.u[(nl - R) & (RLU - 1)][lane + 2];
+        const double a0p = S.u[(nl + R) & (RLU - 1)][lane + 2];
+        const double old = row[lane + 2];
+        const double kp = row[lane + 3];
+        const double km = row[lane + 1];  // new: lane j-1 wrote it last step (lane 0: halo)
+        double s;
+        if (DIM == 3) {
+          const int sp = cp & (RP - 1);
+          const double rm = cr > 0 ? prev : S.up[sp][lane];
+          const double rp = cr < R - 1 ? S.u[(nl + 1) & (RLU - 1)][lane + 2] : S.dn[sp][lane];
+          s = ((((a0m + a0p) + rm) + rp) + km) + kp;
         } else {
-          mine = old;
+          s = ((a0m + a0p) + km) + kp;
         }
+        const double val = (hf + s) * inv;
+        const bool internal = (S.mask[sf] >> lane) & 1u;
+        const double mine = (valid && internal) ? val : old;
+        if (valid) S.u[su][lane + 2] = mine;
         prev = mine;
+        const bool w = ++cr == R;
+        cr = w ? 0 : cr;
+        cp += w;
       }
-      pc.next(R);
       __syncwarp();
 
-      // ---------------- write back the line lane 31 finished --------------
-      const int Ld = t - 31;
-      if (Ld >= 0 && Ld < nLines) {
-        LinePos pd;
-        pd.init(Ld, R);
-        const int64_t n0 = line_node(pd.p, pd.r);
-        if (kval) u[n0 + lane] = S.u[Ld & (RLU - 1)][lane];
-        if (((Ld & 7) == 7) || Ld == nLines - 1) {
+      // ---------------- write back the line lane 31 just finished ---------
+      if (pd.L >= 0 && pd.L < nLines) {
+        if (l16) {
+          const double2 v = *reinterpret_cast<const double2*>(&S.u[pd.L & (RLU - 1)][2 + 2 * lane]);
+          *reinterpret_cast<double2*>(u + pd.off + 2 * lane) = v;
+        }
+        if ((pd.L & 15) == 15 || pd.L == nLines - 1) {
           __syncwarp();
-          if (lane == 0) st_release(myprog, Ld + 1);
+          if (lane0) st_release(myprog, pd.L + 1);
         }
       }
+      pd.next(R, s1, wrap, mrow, mwrap);
     }
     cp_wait<0>();
     __syncwarp();

@@ -89,9 +89,9 @@ __global__ void __launch_bounds__(128) gs_sweep_kernel(GsArgs a) {
         int64_t node;
         if (DIM == 3) {
           const int64_t i0 = p + 1, i1 = 1 + (int64_t)b * a.B1 + r;
-          node = i0 * g.s0 + i1 * g.s1 + k;
+          node = i0 * g.s0 + i1 * g.s1 + k + OFF;
         } else {
-          node = (int64_t)(nl + 1) * g.s0 + k;
+          node = (int64_t)(nl + 1) * g.s0 + k + OFF;
         }
         if (labels[node] == INTERNAL) {
           double s;
