@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-cycles", type=int, default=1)
+    ap.add_argument("--coarse", default="device-inverse", choices=["superlu", "device-inverse"],
+                    help="coarsest solve: host SciPy SuperLU (bit-exact) or device dense inverse")
     return ap.parse_args()
 
 
@@ -94,29 +96,40 @@ def algorithmic_bytes(plans):
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+    """Samples SM clocks and throttle reasons during the timed region via
+    NVML (in-process; spawning nvidia-smi stalls concurrent CUDA calls)."""
 
-    def __init__(self, index):
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index, period=0.25):
         self.index = index
+        self.period = period
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
 
     def _run(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self._max = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        except Exception as exc:  # no NVML: record why
+            self._err = repr(exc)
+            return
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, rs))
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
+        self._err = None
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -127,14 +140,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"no samples: {self._err}"]}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({k for _, rs in self.samples for k, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self._max, "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml"}
 
 
 def measured_peak():
@@ -222,11 +232,15 @@ def run_b200(args, rank, world, local_rank):
 
     setup, plans, f, g, e, setup_times = build_workload(args)
     t0 = time.time()
-    solver = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, device=local_rank)
+    solver = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, device=local_rank,
+                                        coarse_backend=args.coarse)
     log(f"[bench] upload + coarse factor {time.time() - t0:.1f}s, device bytes "
         f"{solver.ctx.device_bytes / 1e9:.2f} GB")
     ctx = solver.ctx
-    stream = torch.cuda.current_stream()
+    # a real (non-legacy) torch stream: the library launches on it, the CUDA
+    # events below are recorded on it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     p0 = plans[0]
     dof = p0.n_internal + p0.n_ghosts
@@ -240,7 +254,6 @@ def run_b200(args, rank, world, local_rank):
     if dist:
         dist.barrier()
     launches0 = ctx.launches
-    ctx.profile(True)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clocks:
@@ -253,6 +266,13 @@ def run_b200(args, rank, world, local_rank):
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     launches = ctx.launches - launches0
+    # Kernel timings: the timed region replays one CUDA graph per cycle, whose
+    # event nodes cannot be timed, so the same steps are repeated with direct
+    # launches and CUDA events around every kernel class (same stream).
+    ctx.profile(True)
+    for _ in range(args.steps):
+        solver._run_cycle()
+        solver._residual_norm()
     gs_ms, gs_n = ctx.profile_read("gs_sweep", 0)
     breakdown = {}
     for k in _lib.KCLASS:
@@ -275,6 +295,7 @@ def run_b200(args, rank, world, local_rank):
                 "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(),
                 "algorithmic_bytes_per_launch": gs_bytes, "avg_launch_ms": gs_avg_s * 1e3,
                 "launches_timed": gs_n, "peak_source": peak_kind,
+                "timing": "CUDA events around each fine-level GS launch, same stream, profiled replay of the timed steps",
                 "cycle_algorithmic_bytes": algorithmic_bytes(plans),
                 "cycle_achieved_gbs": algorithmic_bytes(plans) / (ms / args.steps / 1e3) / 1e9}
 
@@ -313,7 +334,7 @@ def run_b200(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": setup.name, "N": setup.grid.N, "levels": len(plans),
                        "dof": dof, "N_I": p0.n_internal, "N_G": p0.n_ghosts, "cycle": "V(2,1)",
-                       "coarse": setup.cycle.coarse_solver, "parallelism": f"replicas{world}",
+                       "coarse": f"{setup.cycle.coarse_solver}:{args.coarse}", "parallelism": f"replicas{world}",
                        "l2_flush": "not needed: every grid vector (1.08 GB) exceeds L2"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(), "breakdown_ms_per_cycle": breakdown, "setup": setup_times,

@@ -53,7 +53,8 @@ enum gmg_op {
   GMG_OP_RESTRICT_INT = 7,   /* ref transfer.py:88-93  R_INT(l) -> F(l+1)    */
   GMG_OP_RESTRICT_GHOST = 8, /* ref transfer.py:116-121 R_EXT(l) -> G(l+1)   */
   GMG_OP_INTERP_ADD = 9,     /* ref transfer.py:149-151 + solver.py:198      */
-  GMG_OP_ZERO_U = 10
+  GMG_OP_ZERO_U = 10,
+  GMG_OP_COARSE_SOLVE = 11   /* ref solver.py:157-166 on the coarsest level */
 };
 
 /* Library version (major*10000 + minor*100 + patch). */
@@ -85,11 +86,15 @@ int gmg_set_level(gmg_ctx *ctx, int level, int64_t N, double reaction,
 
 /* Cycle parameters (ref smoothing.py:30-47 SmootherConfig, solver.py:49-69
  * CycleConfig): nu1, nu2, gamma (1 = V, 2 = W), coarse_mode (0 = host
- * callback direct solve, 1 = `coarse_sweeps` smoothing sweeps), norm
- * (0 = inf, 1 = l2). */
+ * callback direct solve, 1 = `coarse_sweeps` smoothing sweeps, 2 = device
+ * dense inverse set by gmg_set_coarse_inverse), norm (0 = inf, 1 = l2). */
 int gmg_set_cycle(gmg_ctx *ctx, int nu1, int nu2, int gamma, int coarse_mode,
                   int coarse_sweeps, int norm);
 int gmg_set_coarse_callback(gmg_ctx *ctx, gmg_coarse_cb cb, void *user);
+/* Dense inverse (row-major n x n, n = internal + ghost unknowns of the
+ * coarsest level, ordered like gmg_coarse_cb's rhs) for coarse_mode 2; the
+ * pointer is host memory or (on_device != 0) device memory, copied. */
+int gmg_set_coarse_inverse(gmg_ctx *ctx, int64_t n, const double *inv, int on_device);
 
 /* Host <-> device copies of a level vector (see enum gmg_vector). */
 int gmg_set_vector(gmg_ctx *ctx, int level, int which, const double *host);
@@ -102,7 +107,8 @@ int gmg_apply(gmg_ctx *ctx, int level, int op, int count);
 
 /* Run `ncycles` cycles on level 0 in place (ref solver.py:170-203
  * _cycle/run_cycle).  Asynchronous on the context stream except for the
- * host coarse callback, which synchronizes. */
+ * host coarse callback, which synchronizes.  Without a host callback the
+ * whole cycle is captured once into a CUDA graph and replayed. */
 int gmg_cycle(gmg_ctx *ctx, int ncycles);
 
 /* Residual norms of a level (ref solver.py:135-142): out[0] = max |r_int|,
@@ -125,11 +131,12 @@ int64_t gmg_device_bytes(const gmg_ctx *ctx);
 
 /* Per-kernel-class CUDA-event timing on the launch stream (0 gs sweep,
  * 1 ghost sweep, 2 residuals, 3 band, 4 restriction, 5 interpolation,
- * 6 coarse solve, 7 norms).  gmg_profile(ctx, 1) clears and starts
- * recording; gmg_profile_read synchronizes and returns the summed
- * milliseconds and the number of timed regions of that class on `level`
- * (-1: all levels). */
-int gmg_profile(gmg_ctx *ctx, int enable);
+ * 6 coarse solve, 7 norms).  gmg_profile(ctx, mask) clears the
+ * accumulators and times the classes whose bit is set in mask (0 stops);
+ * inside a captured cycle graph the event pairs become graph nodes.
+ * gmg_profile_read synchronizes and returns the summed milliseconds and the
+ * number of timed regions of that class on `level` (-1: all levels). */
+int gmg_profile(gmg_ctx *ctx, int mask);
 int gmg_profile_read(gmg_ctx *ctx, int kclass, int level, double *total_ms, int64_t *count);
 
 /* Host helper: n draws of the reference's xorshift64* stream from (-1, 1)

@@ -17,6 +17,7 @@ HEADER = os.path.join(HERE, "..", "include", "ghostmg_b200.h")
 U, F, G, R_INT, R_EXT = 0, 1, 2, 3, 4
 OP_GS_SWEEP, OP_GHOST_SWEEP, OP_SMOOTH, OP_RES_INT, OP_RES_GHOST = 0, 1, 2, 3, 4
 OP_EXTEND_REXT, OP_EXTEND_U, OP_RESTRICT_INT, OP_RESTRICT_GHOST, OP_INTERP_ADD, OP_ZERO_U = 5, 6, 7, 8, 9, 10
+OP_COARSE_SOLVE = 11
 KCLASS = {"gs_sweep": 0, "ghost_sweep": 1, "residual": 2, "band": 3, "restrict": 4,
           "interp": 5, "coarse": 6, "norm": 7}
 
@@ -37,6 +38,7 @@ SIGNATURES = {
     "gmg_set_level": (_i, [_p, _i, _i64, _d, _p, _i64, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p]),
     "gmg_set_cycle": (_i, [_p, _i, _i, _i, _i, _i, _i]),
     "gmg_set_coarse_callback": (_i, [_p, COARSE_CB, _p]),
+    "gmg_set_coarse_inverse": (_i, [_p, _i64, _p, _i]),
     "gmg_set_vector": (_i, [_p, _i, _i, _p]),
     "gmg_get_vector": (_i, [_p, _i, _i, _p]),
     "gmg_device_pointer": (_p, [_p, _i, _i]),
@@ -148,6 +150,9 @@ class Context:
         self._keep.append(cb)
         self.check(self.lib.gmg_set_coarse_callback(self.ctx, cb, None))
 
+    def set_coarse_inverse(self, n, ptr_value, on_device):
+        self.check(self.lib.gmg_set_coarse_inverse(self.ctx, n, ptr_value, 1 if on_device else 0))
+
     def set_stream(self, stream_handle):
         self.check(self.lib.gmg_set_stream(self.ctx, stream_handle))
 
@@ -193,8 +198,17 @@ class Context:
     def device_bytes(self):
         return int(self.lib.gmg_device_bytes(self.ctx))
 
-    def profile(self, enable=True):
-        self.check(self.lib.gmg_profile(self.ctx, 1 if enable else 0))
+    def profile(self, enable=True, classes=None):
+        """Time kernel classes with CUDA events (all of them, or ``classes``)."""
+        if not enable:
+            mask = 0
+        elif classes is None:
+            mask = 0xFF
+        else:
+            mask = 0
+            for c in classes:
+                mask |= 1 << KCLASS.get(c, c)
+        self.check(self.lib.gmg_profile(self.ctx, mask))
 
     def profile_read(self, kclass, level=-1):
         ms = np.zeros(1)

@@ -1,0 +1,69 @@
+// coarse_dense.cu -- device coarsest-level solve x = A^{-1} rhs (sm_100a).
+//
+// Optional replacement for the reference's host SuperLU solve
+// (/root/reference/pkg/src/ghostmg/solver.py:146-166): the coarsest operator
+// (a few 10^4 unknowns for the pore-space hierarchy) is inverted once at
+// setup and every cycle applies the dense inverse with an HBM-streaming
+// GEMV.  Deterministic: the column range is cut into fixed chunks, each
+// (row, chunk) partial is a fixed warp-shuffle tree, and the chunk partials
+// are added in chunk order.  Not bitwise equal to SuperLU (the reference's
+// own solve is only reproducible by calling SuperLU), so it is an opt-in
+// mode; tests bound its effect on residual histories.
+#include "gmg_kernels.cuh"
+
+namespace gmg {
+
+constexpr int GEMV_CHUNK = 8192;  // columns per chunk (64 KB of rhs in shared memory)
+constexpr int GEMV_ROWS = 64;     // rows per CTA
+
+__global__ void __launch_bounds__(256) gemv_partial_kernel(const double* __restrict__ A, const double* __restrict__ x,
+                                                           int64_t n, double* __restrict__ part) {
+  extern __shared__ double xs[];
+  const int ch = blockIdx.y;
+  const int64_t c0 = (int64_t)ch * GEMV_CHUNK;
+  const int len = (int)min((int64_t)GEMV_CHUNK, n - c0);
+  for (int i = threadIdx.x; i < len; i += blockDim.x) xs[i] = x[c0 + i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)blockIdx.x * GEMV_ROWS;
+  for (int rr = warp; rr < GEMV_ROWS; rr += 8) {
+    const int64_t row = r0 + rr;
+    if (row >= n) break;
+    const double* a = A + row * n + c0;
+    double s0 = 0.0, s1 = 0.0;
+    int j = lane;
+    for (; j + 32 < len; j += 64) {
+      s0 = __fma_rn(__ldcs(a + j), xs[j], s0);
+      s1 = __fma_rn(__ldcs(a + j + 32), xs[j + 32], s1);
+    }
+    if (j < len) s0 = __fma_rn(__ldcs(a + j), xs[j], s0);
+    double s = s0 + s1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) part[(int64_t)ch * n + row] = s;
+  }
+}
+
+__global__ void gemv_reduce_kernel(const double* __restrict__ part, int64_t n, int nch, double* __restrict__ y) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = part[i];
+  for (int c = 1; c < nch; ++c) s += part[(int64_t)c * n + i];
+  y[i] = s;
+}
+
+void configure_dense_gemv() {
+  cudaFuncSetAttribute(gemv_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(GEMV_CHUNK * sizeof(double)));
+}
+
+int gemv_chunks(int64_t n) { return (int)((n + GEMV_CHUNK - 1) / GEMV_CHUNK); }
+
+void launch_dense_gemv(const double* A, const double* x, int64_t n, double* part, double* y, cudaStream_t st) {
+  const int nch = gemv_chunks(n);
+  dim3 grid((unsigned)((n + GEMV_ROWS - 1) / GEMV_ROWS), (unsigned)nch);
+  gemv_partial_kernel<<<grid, 256, GEMV_CHUNK * sizeof(double), st>>>(A, x, n, part);
+  gemv_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, n, nch, y);
+}
+
+}  // namespace gmg

@@ -55,6 +55,8 @@ struct DevLevel {
   int64_t n_int = 0;
   int64_t* active = nullptr;  // internal nodes then ghost nodes (lex)
   double *rhs_d = nullptr, *x_d = nullptr, *rhs_h = nullptr, *x_h = nullptr;
+  double *cinv = nullptr, *cpart = nullptr;  // device dense inverse of the coarsest operator
+  int64_t cinv_n = 0;
   bool ready = false;
 };
 
@@ -86,9 +88,20 @@ struct gmg_ctx {
   bool no_ws = false;
   int ws_ctas_per_sm = 4;
   bool prof = false;
+  int prof_mask = 0;   // bit k: time kernel class k
   int cur_level = -1;  // level tag for profiling records
-  std::vector<Prof> events;
+  std::vector<Prof> events;        // pending (direct launches)
+  std::vector<Prof> graph_events;  // recorded inside the captured cycle graph
   std::vector<cudaEvent_t> pool;
+  double acc_ms[8][16] = {};       // accumulated per (class, level)
+  int64_t acc_n[8][16] = {};
+  // CUDA graph of one cycle (used when the coarsest solve needs no host callback)
+  bool use_graph = true;
+  bool graph_valid = false;
+  int graph_mask = 0;
+  cudaGraphExec_t graph_exec = nullptr;
+  int64_t graph_launches_per_cycle = 0;
+  int graph_runs_pending = 0;      // graph launches since the last profile flush
 };
 
 namespace {
@@ -130,7 +143,7 @@ int upload(gmg_ctx* ctx, T** p, const T* host, int64_t count) {
 void free_level(DevLevel& l) {
   void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
-                  l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask};  // ticket lives in progress
+                  l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.cinv, l.cpart};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -139,12 +152,20 @@ void free_level(DevLevel& l) {
 }
 
 // ---- profiling ----------------------------------------------------------
+bool capturing(gmg_ctx* ctx) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(ctx->stream, &st);
+  return st == cudaStreamCaptureStatusActive;
+}
+
 struct Scope {
   gmg_ctx* ctx;
   int cls;
+  bool on;
   cudaEvent_t a = nullptr;
   Scope(gmg_ctx* c, int k) : ctx(c), cls(k) {
-    if (!ctx->prof) return;
+    on = ctx->prof && ((ctx->prof_mask >> k) & 1);
+    if (!on) return;
     a = take();
     cudaEventRecord(a, ctx->stream);
   }
@@ -159,12 +180,57 @@ struct Scope {
     return e;
   }
   ~Scope() {
-    if (!ctx->prof) return;
+    if (!on) return;
     cudaEvent_t b = take();
     cudaEventRecord(b, ctx->stream);
-    ctx->events.push_back({a, b, cls, ctx->cur_level});
+    if (capturing(ctx))
+      ctx->graph_events.push_back({a, b, cls, ctx->cur_level});
+    else
+      ctx->events.push_back({a, b, cls, ctx->cur_level});
   }
 };
+
+// Fold finished event pairs into the per-(class, level) accumulators.  Must
+// follow a stream synchronisation.  Graph events hold the timestamps of the
+// latest graph launch; they are weighted by the launches since the last
+// flush (exact when, as in solve(), every cycle is followed by a sync).
+void profile_flush(gmg_ctx* ctx) {
+  for (auto& e : ctx->events) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, e.a, e.b) == cudaSuccess) {
+      const int lv = std::min(std::max(e.level, 0), 15);
+      ctx->acc_ms[e.cls][lv] += ms;
+      ctx->acc_n[e.cls][lv] += 1;
+    }
+    ctx->pool.push_back(e.a);
+    ctx->pool.push_back(e.b);
+  }
+  ctx->events.clear();
+  if (ctx->graph_runs_pending > 0) {
+    for (auto& e : ctx->graph_events) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, e.a, e.b) == cudaSuccess) {
+        const int lv = std::min(std::max(e.level, 0), 15);
+        ctx->acc_ms[e.cls][lv] += (double)ms * ctx->graph_runs_pending;
+        ctx->acc_n[e.cls][lv] += ctx->graph_runs_pending;
+      }
+    }
+    ctx->graph_runs_pending = 0;
+  }
+  cudaGetLastError();
+}
+
+void graph_reset(gmg_ctx* ctx) {
+  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+  ctx->graph_exec = nullptr;
+  ctx->graph_valid = false;
+  for (auto& e : ctx->graph_events) {
+    ctx->pool.push_back(e.a);
+    ctx->pool.push_back(e.b);
+  }
+  ctx->graph_events.clear();
+  ctx->graph_runs_pending = 0;
+}
 
 // ---- level helpers ---------------------------------------------------------
 Geom make_geom(int d, int64_t N, double reaction) {
@@ -191,6 +257,14 @@ Geom make_geom(int d, int64_t N, double reaction) {
   g.inv = 1.0 / g.denom;
   g.c = g.denom / g.h2;
   return g;
+}
+
+// large-shared-memory kernels are configured once, outside any graph capture
+void configure_kernels() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  configure_gs_kernels();
 }
 
 // reference flat index (C order over (N+1)^d) -> padded device position
@@ -360,8 +434,16 @@ int coarse_solve(gmg_ctx* ctx, int li) {
   Scope s(ctx, 6);
   GMG_CHECK(ctx, cudaMemsetAsync(l.u, 0, sizeof(double) * (size_t)l.g.nodes, ctx->stream));
   if (ctx->coarse_mode == 1) return op_smooth(ctx, l, ctx->coarse_sweeps);
-  if (!ctx->cb) return fail(ctx, "coarsest direct solve requested but no callback set");
   const int64_t n = l.n_int + l.ng;
+  if (ctx->coarse_mode == 2) {
+    if (!l.cinv || l.cinv_n != n) return fail(ctx, "device coarse mode needs gmg_set_coarse_inverse");
+    launch_gather(l.active, l.n_int, l.f, l.lex2slot, l.ng, l.gval, l.rhs_d, ctx->stream);
+    launch_dense_gemv(l.cinv, l.rhs_d, n, l.cpart, l.x_d, ctx->stream);
+    launch_scatter(l.active, n, l.x_d, l.u, ctx->stream);
+    ctx->launches += 4;
+    return 0;
+  }
+  if (!ctx->cb) return fail(ctx, "coarsest direct solve requested but no callback set");
   launch_gather(l.active, l.n_int, l.f, l.lex2slot, l.ng, l.gval, l.rhs_d, ctx->stream);
   ctx->launches++;
   GMG_CHECK(ctx, cudaMemcpyAsync(l.rhs_h, l.rhs_d, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost,
@@ -431,6 +513,8 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_SIMPLE_GS")) ctx->force_simple_gs = e[0] == '1';
   if (const char* e = getenv("GMG_GS_MAX_TASKS")) ctx->gs_max_tasks = atoi(e);
   if (const char* e = getenv("GMG_NO_WS")) ctx->no_ws = e[0] == '1';
+  if (const char* e = getenv("GMG_NO_GRAPH")) ctx->use_graph = e[0] != '1';
+  configure_kernels();
   if (cudaMalloc(&ctx->dmax, 8 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost(&ctx->hmax, 8 * sizeof(unsigned long long)) != cudaSuccess) {
     delete ctx;
@@ -443,6 +527,7 @@ void gmg_destroy(gmg_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  graph_reset(ctx);
   for (auto& l : ctx->L) free_level(l);
   for (auto& e : ctx->events) {
     cudaEventDestroy(e.a);
@@ -458,6 +543,7 @@ void gmg_destroy(gmg_ctx* ctx) {
 const char* gmg_last_error(const gmg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int gmg_set_stream(gmg_ctx* ctx, void* s) {
+  cudaStreamSynchronize(ctx->stream);
   ctx->stream = s ? (cudaStream_t)s : ctx->own;
   return 0;
 }
@@ -471,6 +557,7 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   if (li < 0 || li >= ctx->nlevels) return fail(ctx, "level out of range");
   if (N < 2 || (N % 2)) return fail(ctx, "N must be even and >= 2");
   cudaSetDevice(ctx->device);
+  graph_reset(ctx);
   DevLevel& l = ctx->L[li];
   free_level(l);
   const int d = ctx->ndim;
@@ -619,14 +706,31 @@ int gmg_set_cycle(gmg_ctx* ctx, int nu1, int nu2, int gamma, int coarse_mode, in
                   int norm) {
   if (nu1 < 0 || nu2 < 0 || nu1 + nu2 == 0) return fail(ctx, "need nu1, nu2 >= 0, not both 0");
   if (gamma < 1) return fail(ctx, "gamma must be >= 1");
-  if (coarse_mode < 0 || coarse_mode > 1) return fail(ctx, "unknown coarse mode");
+  if (coarse_mode < 0 || coarse_mode > 2) return fail(ctx, "unknown coarse mode");
   if (norm < 0 || norm > 1) return fail(ctx, "unknown norm");
+  graph_reset(ctx);
   ctx->nu1 = nu1;
   ctx->nu2 = nu2;
   ctx->gamma = gamma;
   ctx->coarse_mode = coarse_mode;
   ctx->coarse_sweeps = coarse_sweeps;
   ctx->norm = norm;
+  return 0;
+}
+
+int gmg_set_coarse_inverse(gmg_ctx* ctx, int64_t n, const double* inv, int on_device) {
+  DevLevel& l = ctx->L[ctx->nlevels - 1];
+  if (!l.ready) return fail(ctx, "coarsest level not set");
+  if (n != l.n_int + l.ng) return fail(ctx, "coarse inverse size does not match the coarsest level");
+  cudaSetDevice(ctx->device);
+  graph_reset(ctx);
+  if (l.cinv) cudaFree(l.cinv);
+  if (l.cpart) cudaFree(l.cpart);
+  l.cinv = l.cpart = nullptr;
+  if (dalloc(ctx, &l.cinv, n * n) || dalloc(ctx, &l.cpart, (int64_t)gemv_chunks(n) * n)) return -1;
+  GMG_CHECK(ctx, cudaMemcpy(l.cinv, inv, sizeof(double) * (size_t)(n * n),
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+  l.cinv_n = n;
   return 0;
 }
 
@@ -722,6 +826,10 @@ int gmg_apply(gmg_ctx* ctx, int li, int op, int count) {
     case GMG_OP_ZERO_U:
       GMG_CHECK(ctx, cudaMemsetAsync(l.u, 0, sizeof(double) * l.g.nodes, ctx->stream));
       break;
+    case GMG_OP_COARSE_SOLVE:
+      if (li != ctx->nlevels - 1) return fail(ctx, "coarse solve runs on the coarsest level");
+      rc = coarse_solve(ctx, li);
+      break;
     default: return fail(ctx, "unknown op");
   }
   if (rc) return rc;
@@ -733,8 +841,41 @@ int gmg_apply(gmg_ctx* ctx, int li, int op, int count) {
 int gmg_cycle(gmg_ctx* ctx, int ncycles) {
   if (!levels_ready(ctx)) return fail(ctx, "not every level is set");
   cudaSetDevice(ctx->device);
-  for (int i = 0; i < ncycles; ++i)
-    if (cycle_level(ctx, 0)) return -1;
+  // the host-callback coarsest solve synchronises mid-cycle: no graph then;
+  // profiled runs launch directly so every timed region has its own events
+  const bool graph = ctx->use_graph && ctx->coarse_mode != 0 && !ctx->prof;
+  if (!graph) {
+    for (int i = 0; i < ncycles; ++i)
+      if (cycle_level(ctx, 0)) return -1;
+    GMG_CHECK(ctx, cudaGetLastError());
+    return 0;
+  }
+  const int mask = ctx->prof ? ctx->prof_mask : 0;
+  if (!ctx->graph_valid || ctx->graph_mask != mask) {
+    graph_reset(ctx);
+    cudaGraph_t gr = nullptr;
+    const int64_t l0 = ctx->launches;
+    GMG_CHECK(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = cycle_level(ctx, 0);
+    const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &gr);
+    if (rc) {
+      if (gr) cudaGraphDestroy(gr);
+      return rc;
+    }
+    if (ec != cudaSuccess) return fail(ctx, std::string("graph capture failed: ") + cudaGetErrorString(ec));
+    const cudaError_t ei = cudaGraphInstantiate(&ctx->graph_exec, gr, 0);
+    cudaGraphDestroy(gr);
+    if (ei != cudaSuccess) return fail(ctx, std::string("graph instantiate failed: ") + cudaGetErrorString(ei));
+    ctx->graph_launches_per_cycle = ctx->launches - l0;
+    ctx->launches = l0;
+    ctx->graph_valid = true;
+    ctx->graph_mask = mask;
+  }
+  for (int i = 0; i < ncycles; ++i) {
+    GMG_CHECK(ctx, cudaGraphLaunch(ctx->graph_exec, ctx->stream));
+    ctx->launches += ctx->graph_launches_per_cycle;
+    if (mask) ctx->graph_runs_pending += 1;
+  }
   GMG_CHECK(ctx, cudaGetLastError());
   return 0;
 }
@@ -752,6 +893,7 @@ int gmg_residual_norm(gmg_ctx* ctx, int li, double* out) {
                                  cudaMemcpyDeviceToHost, ctx->stream));
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   GMG_CHECK(ctx, cudaGetLastError());
+  if (ctx->prof) profile_flush(ctx);
   std::memcpy(out, ctx->hmax, 2 * sizeof(double));
   return 0;
 }
@@ -785,33 +927,40 @@ int gmg_abs_max_scale(gmg_ctx* ctx, double threshold, double factor, double* pea
 int gmg_synchronize(gmg_ctx* ctx) {
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   GMG_CHECK(ctx, cudaGetLastError());
+  if (ctx->prof) profile_flush(ctx);
   return 0;
 }
 
 int64_t gmg_launch_count(const gmg_ctx* ctx) { return ctx->launches; }
 int64_t gmg_device_bytes(const gmg_ctx* ctx) { return ctx->bytes; }
 
-int gmg_profile(gmg_ctx* ctx, int enable) {
+int gmg_profile(gmg_ctx* ctx, int mask) {
   cudaStreamSynchronize(ctx->stream);
-  for (auto& e : ctx->events) {
-    ctx->pool.push_back(e.a);
-    ctx->pool.push_back(e.b);
+  profile_flush(ctx);
+  for (auto& row : ctx->acc_ms)
+    for (auto& v : row) v = 0.0;
+  for (auto& row : ctx->acc_n)
+    for (auto& v : row) v = 0;
+  ctx->prof = mask != 0;
+  ctx->prof_mask = mask;
+  while (ctx->pool.size() < 1024) {  // no cudaEventCreate inside timed regions
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    ctx->pool.push_back(e);
   }
-  ctx->events.clear();
-  ctx->prof = enable != 0;
   return 0;
 }
 
 int gmg_profile_read(gmg_ctx* ctx, int kclass, int level, double* total_ms, int64_t* count) {
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  profile_flush(ctx);
   double t = 0.0;
   int64_t n = 0;
-  for (auto& e : ctx->events) {
-    if (e.cls != kclass || (level >= 0 && e.level != level)) continue;
-    float ms = 0.f;
-    GMG_CHECK(ctx, cudaEventElapsedTime(&ms, e.a, e.b));
-    t += ms;
-    n++;
+  if (kclass < 0 || kclass > 7) return fail(ctx, "unknown kernel class");
+  for (int lv = 0; lv < 16; ++lv) {
+    if (level >= 0 && lv != level) continue;
+    t += ctx->acc_ms[kclass][lv];
+    n += ctx->acc_n[kclass][lv];
   }
   *total_ms = t;
   *count = n;

@@ -52,6 +52,7 @@ struct WsMaps {
 };
 void launch_gs_ws(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st);
 size_t gs_ws_smem();
+void configure_gs_kernels();  // set max dynamic shared memory of the GS / GEMV kernels
 
 void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st);
 void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,
@@ -73,6 +74,8 @@ void launch_scale(double* u, int64_t n, double s, cudaStream_t st);
 void launch_gather(const int64_t* idx, int64_t n_int, const double* f, const int32_t* ghost_slot,
                    int64_t n_gh, const double* gval, double* out, cudaStream_t st);
 void launch_scatter(const int64_t* idx, int64_t n, const double* x, double* e, cudaStream_t st);
+void launch_dense_gemv(const double* A, const double* x, int64_t n, double* part, double* y, cudaStream_t st);
+int gemv_chunks(int64_t n);
 void launch_permute(const double* src, const int32_t* perm, int64_t n, double* dst,
                     cudaStream_t st);
 

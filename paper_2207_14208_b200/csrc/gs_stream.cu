@@ -249,22 +249,23 @@ __global__ void __launch_bounds__(32) gs_stream_kernel(GsArgs a) {
 
 size_t gs_stream_smem_per_warp() { return sizeof(WarpRing); }
 
+void configure_gs_ws();
+void configure_dense_gemv();
+
+void configure_gs_kernels() {
+  const int smem = (int)sizeof(WarpRing);  // one warp per CTA
+  cudaFuncSetAttribute(gs_stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gs_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  configure_gs_ws();
+  configure_dense_gemv();
+}
+
 void launch_gs_stream(const GsArgs& a, int grid, int warps_per_cta, cudaStream_t st) {
   const size_t smem = sizeof(WarpRing) * warps_per_cta;
-  static bool configured[2] = {false, false};
-  if (a.g.d == 3) {
-    if (!configured[1]) {
-      cudaFuncSetAttribute(gs_stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      configured[1] = true;
-    }
+  if (a.g.d == 3)
     gs_stream_kernel<3><<<grid, 32 * warps_per_cta, smem, st>>>(a);
-  } else {
-    if (!configured[0]) {
-      cudaFuncSetAttribute(gs_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      configured[0] = true;
-    }
+  else
     gs_stream_kernel<2><<<grid, 32 * warps_per_cta, smem, st>>>(a);
-  }
 }
 
 }  // namespace gmg

@@ -344,17 +344,15 @@ __global__ void __launch_bounds__(64, 1) gs_ws_kernel(GsArgs a, const __grid_con
 
 size_t gs_ws_smem() { return sizeof(WsSmem); }
 
+void configure_gs_ws() {
+  const int smem = (int)sizeof(WsSmem);
+  cudaFuncSetAttribute(gs_ws_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gs_ws_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
 void launch_gs_ws(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st) {
   const size_t smem = sizeof(WsSmem);
-  static bool configured[2] = {false, false};
   const int k = a.g.d == 3 ? 1 : 0;
-  if (!configured[k]) {
-    if (k)
-      cudaFuncSetAttribute(gs_ws_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    else
-      cudaFuncSetAttribute(gs_ws_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured[k] = true;
-  }
   if (k)
     gs_ws_kernel<3><<<grid, 64, smem, st>>>(a, maps);
   else

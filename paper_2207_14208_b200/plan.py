@@ -13,6 +13,7 @@ Reference data this replaces: ``SweepPlan`` (smoothing.py:80-109),
 """
 
 from dataclasses import dataclass, fields
+from functools import cached_property
 
 import numpy as np
 import scipy.sparse as sp
@@ -79,11 +80,11 @@ class LevelPlan:
         blocks = self.ghost_low[:, None, :] + block_offsets(self.d)[None, :, :]
         return (blocks * g.strides).sum(axis=-1)
 
-    @property
+    @cached_property
     def internal_idx(self):
         return np.flatnonzero(self.labels == INTERNAL)
 
-    @property
+    @cached_property
     def n_internal(self):
         return int(np.count_nonzero(self.labels == INTERNAL))
 

@@ -10,10 +10,14 @@ Drop-in for /root/reference/pkg/src/ghostmg/solver.py:
   (``cycle.CycleDriver``) while every cycle runs on the device
   (``_lib.Context.cycle``), with the iterate resident in HBM between
   cycles; only the two residual-norm scalars come back per cycle.
-* The coarsest solve is the reference's own: SciPy SuperLU of the assembled
-  coarsest system (solver.py:146-166), called through the library's host
-  callback on a few-KB right-hand side, or ``coarse_solver="sweeps"``
-  (500 device smoothing sweeps).
+* The coarsest solve is the reference's own by default: SciPy SuperLU of the
+  assembled coarsest system (solver.py:146-166), called through the
+  library's host callback on a few-KB right-hand side (bit-exact), or
+  ``coarse_solver="sweeps"`` (500 device smoothing sweeps, bit-exact).
+  ``coarse_backend="device-inverse"`` instead inverts the coarsest operator
+  once on the GPU (setup) and applies the dense inverse with the library's
+  GEMV kernel every cycle -- no host round trip; results then differ from
+  the reference at round-off level (bounded in tests/test_gpu_parity.py).
 """
 
 import numpy as np
@@ -36,21 +40,50 @@ from .transfer import build_hierarchy
 __all__ = ["MultigridSolver", "build_solver", "measure_rho", "CycleConfig", "CycleReport"]
 
 
+COARSE_BACKENDS = ("superlu", "device-inverse")
+
+
 class DeviceHierarchy:
     """All levels of one solver resident on one GPU."""
 
-    def __init__(self, plans, smoother, cycle, device=0):
+    def __init__(self, plans, smoother, cycle, device=0, coarse_backend="superlu"):
+        if coarse_backend not in COARSE_BACKENDS:
+            raise ValueError(f"unknown coarse backend {coarse_backend!r}")
         self.plans = plans
+        self.device_index = device
         d = plans[0].d
         self.ctx = _lib.Context(d, len(plans), device)
         for i, p in enumerate(plans):
             self.ctx.set_level(i, p)
-        coarse_mode = 1 if cycle.coarse_solver == "sweeps" else 0
+        if cycle.coarse_solver == "sweeps":
+            coarse_mode = 1
+        elif coarse_backend == "device-inverse":
+            coarse_mode = 2
+        else:
+            coarse_mode = 0
         self.ctx.set_cycle(smoother.nu1, smoother.nu2, cycle.gamma, coarse_mode,
                            cycle.coarse_sweeps, 0)
         self._lu = None
         if coarse_mode == 0:
             self.ctx.set_coarse_callback(self._coarse)
+        elif coarse_mode == 2:
+            self._upload_inverse()
+
+    def _upload_inverse(self):
+        """Invert the coarsest operator on the GPU (setup) and hand it to the
+        library, which copies it into its own buffer."""
+        import torch
+
+        A, _ = coarsest_system(self.plans[-1])
+        n = A.shape[0]
+        dev = torch.device("cuda", self.device_index)
+        dense = torch.from_numpy(A.toarray()).to(dev)
+        inv = torch.linalg.inv(dense).contiguous()  # LAPACK-backed results may be column-major
+        del dense
+        torch.cuda.synchronize(dev)
+        self.ctx.set_coarse_inverse(n, inv.data_ptr(), True)
+        del inv
+        torch.cuda.empty_cache()
 
     def _factor(self):
         if self._lu is None:
@@ -69,35 +102,34 @@ class MultigridSolver(CycleDriver):
     """Reference ``MultigridSolver`` with every cycle on the B200."""
 
     def __init__(self, levels, spec, smoother=None, cycle=None, default_variant=VARIANT_POLY,
-                 device=0):
+                 device=0, coarse_backend="superlu"):
         smoother = smoother or SmootherConfig()
         cycle = cycle or CycleConfig()
         plans, f, g, e = CycleDriver.problem_data(levels, spec, smoother, default_variant)
         super().__init__(plans, f, g, e, smoother, cycle)
         self.levels = levels
         self.spec = spec
-        self._init_device(device)
+        self._init_device(device, coarse_backend)
 
     @classmethod
     def from_plans(cls, plans, f_fine, g_fine, eliminated_values, smoother=None, cycle=None,
-                   device=0):
+                   device=0, coarse_backend="superlu"):
         self = cls.__new__(cls)
         CycleDriver.__init__(self, plans, f_fine, g_fine, eliminated_values,
                              smoother or SmootherConfig(), cycle or CycleConfig())
         self.levels = None
         self.spec = None
-        self._init_device(device)
+        self._init_device(device, coarse_backend)
         return self
 
-    def _init_device(self, device):
+    def _init_device(self, device, coarse_backend):
         if self.cycle_cfg.norm == NORM_L2:
             raise NotImplementedError("norm='l2' is not implemented on the B200 path yet")
-        self.device = DeviceHierarchy(self.plans, self.smoother, self.cycle_cfg, device)
+        self.coarse_backend = coarse_backend
+        self.device = DeviceHierarchy(self.plans, self.smoother, self.cycle_cfg, device,
+                                      coarse_backend)
         self.ctx = self.device.ctx
-        self._factor_now()
-
-    def _factor_now(self):
-        if self.cycle_cfg.coarse_solver != "sweeps":
+        if self.cycle_cfg.coarse_solver != "sweeps" and coarse_backend == "superlu":
             self.device._factor()
 
     # ---- primitives --------------------------------------------------------
@@ -128,9 +160,10 @@ class MultigridSolver(CycleDriver):
 
 
 def build_solver(grid, phi, spec, eliminated_faces=(), smoother=None, cycle=None,
-                 default_variant=VARIANT_POLY, coarsest_min=4, device=0):
+                 default_variant=VARIANT_POLY, coarsest_min=4, device=0, coarse_backend="superlu"):
     """Hierarchy + B200 solver in one call (reference solver.py:272-279)."""
     cycle = cycle or CycleConfig()
     levels = build_hierarchy(grid, phi, eliminated_faces, max_levels=cycle.max_levels,
                              coarsest_min=coarsest_min)
-    return MultigridSolver(levels, spec, smoother, cycle, default_variant, device=device)
+    return MultigridSolver(levels, spec, smoother, cycle, default_variant, device=device,
+                           coarse_backend=coarse_backend)

@@ -106,3 +106,51 @@ def test_device_solve_matches_reference(name, gpu_available):
         r = measure_rho(solver, seed=42)
         assert r.residual_norms == GU.hexlist(rec["rho"]["residual_norms"])
         assert r.rho_asymptotic == rec["rho"]["rho"]
+
+
+def _pores64_solver(coarse_backend):
+    from paper_2207_14208_b200 import configs as CF
+    from paper_2207_14208_b200.cycle import CycleDriver
+    from paper_2207_14208_b200.transfer import build_hierarchy
+
+    setup = CF.config_pores(N=64, cycles=15)
+    levels = build_hierarchy(setup.grid, setup.phi, setup.faces, coarsest_min=setup.coarsest_min)
+    plans, f, g, e = CycleDriver.problem_data(levels, setup.spec, setup.smoother, setup.default_variant)
+    f = CF.pore_rhs(setup, plans[0].labels)
+    return plans, MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle,
+                                             coarse_backend=coarse_backend)
+
+
+def test_pores64_setup_and_solve_match_reference(gpu_available):
+    """Host setup rebuilt here must hash like the reference's plans, and the
+    device solve (host SuperLU coarsest) must reproduce the reference."""
+    rec = GU.record("pores64")
+    plans, solver = _pores64_solver("superlu")
+    for lvl, p in enumerate(plans):
+        got = {k: GU.plan_digest(v) for k, v in p.to_arrays().items()}
+        assert got == rec["plan_digests"][lvl]
+    u, rep = solver.solve(u=np.zeros(plans[0].n_nodes), cycles=rec["cycles"])
+    assert rep.residual_norms == GU.hexlist(rec["solve"]["residual_norms"])
+    assert GU.digest(u) == rec["solve"]["u_digest"]
+    assert measure_rho(solver, seed=42).rho_asymptotic == rec["rho"]["rho"]
+
+
+def test_device_inverse_coarse_solve_within_tolerance(gpu_available):
+    """coarse_backend='device-inverse' is not bitwise (a dense inverse is not
+    SuperLU).  Its round-off difference is amplified relative to the residual
+    as the residual falls towards the floating-point floor (SURVEY.md
+    finding 4), so per-cycle residual norms are held to 1e-10 relative while
+    the residual is above 1e-6 of its start; the final iterate to 1e-12
+    relative L-inf and rho to 1e-3 (the north-star tolerances)."""
+    rec = GU.record("pores64")
+    plans, solver = _pores64_solver("device-inverse")
+    u, rep = solver.solve(u=np.zeros(plans[0].n_nodes), cycles=rec["cycles"])
+    want = np.array(GU.hexlist(rec["solve"]["residual_norms"]))
+    got = np.array(rep.residual_norms)
+    early = want > 1e-6 * want[0]
+    assert early.sum() >= 6
+    assert np.max(np.abs(got - want)[early] / want[early]) < 1e-10
+    _, ref = _pores64_solver("superlu")
+    uref, _ = ref.solve(u=np.zeros(plans[0].n_nodes), cycles=rec["cycles"])
+    assert np.max(np.abs(u - uref)) <= 1e-12 * np.max(np.abs(uref))
+    assert abs(measure_rho(solver, seed=42).rho_asymptotic - rec["rho"]["rho"]) < 1e-3
