@@ -137,17 +137,19 @@ def test_pores64_setup_and_solve_match_reference(gpu_available):
 
 def test_device_inverse_coarse_solve_within_tolerance(gpu_available):
     """coarse_backend='device-inverse' is not bitwise (a dense inverse is not
-    SuperLU).  Its round-off difference is amplified relative to the residual
-    as the residual falls towards the floating-point floor (SURVEY.md
-    finding 4), so per-cycle residual norms are held to 1e-10 relative while
-    the residual is above 1e-6 of its start; the final iterate to 1e-12
-    relative L-inf and rho to 1e-3 (the north-star tolerances)."""
+    SuperLU).  Its per-cycle round-off (~1e-15 of the correction) stays fixed
+    in absolute size while the residual falls by rho per cycle, so the
+    relative difference of the residual norms grows like 1e-15 / (r_m / r_0)
+    (SURVEY.md finding 4).  Per-cycle norms are held to 1e-10 relative while
+    r_m / r_0 > 1e-4; the final iterate to 1e-12 relative L-inf and rho to
+    1e-3 (the north-star tolerances).  The default coarse backend (host
+    SuperLU) is bitwise: see test_pores64_setup_and_solve_match_reference."""
     rec = GU.record("pores64")
     plans, solver = _pores64_solver("device-inverse")
     u, rep = solver.solve(u=np.zeros(plans[0].n_nodes), cycles=rec["cycles"])
     want = np.array(GU.hexlist(rec["solve"]["residual_norms"]))
     got = np.array(rep.residual_norms)
-    early = want > 1e-6 * want[0]
+    early = want > 1e-4 * want[0]
     assert early.sum() >= 6
     assert np.max(np.abs(got - want)[early] / want[early]) < 1e-10
     _, ref = _pores64_solver("superlu")
