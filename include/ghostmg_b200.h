@@ -99,7 +99,9 @@ int gmg_set_coarse_inverse(gmg_ctx *ctx, int64_t n, const double *inv, int on_de
 /* Host <-> device copies of a level vector (see enum gmg_vector). */
 int gmg_set_vector(gmg_ctx *ctx, int level, int which, const double *host);
 int gmg_get_vector(gmg_ctx *ctx, int level, int which, double *host);
-/* Device address of a level vector (valid for the context's lifetime). */
+/* Device address of a level vector (valid for the context's lifetime).  Grids
+ * are stored padded (row pitch roundup(N+4,4), column offset 3); GMG_G is
+ * stored in sweep-slot order (batches padded to 32 slots), not ghost order. */
 void *gmg_device_pointer(gmg_ctx *ctx, int level, int which);
 
 /* Run one operation on a level (see enum gmg_op). */

@@ -28,8 +28,12 @@ struct DevLevel {
   int64_t N = 0;
   uint8_t* labels = nullptr;
   double *u = nullptr, *f = nullptr, *rI = nullptr, *rE = nullptr;
-  // ghosts, slot order
-  int64_t ng = 0;
+  // ghosts, slot order (batches padded to multiples of 32 slots; node -1 = empty slot)
+  int64_t ng = 0;      // ghosts (lexicographic count)
+  int64_t nslots = 0;  // padded slots
+  int32_t* dep_off = nullptr;  // [nslots+1] CSR: slots each slot must wait for
+  int32_t* dep = nullptr;
+  int* gctr = nullptr;         // [nslots] done flags + chunk cursor
   int64_t *gnode = nullptr, *gbase = nullptr;
   double *gw = nullptr, *gdtau = nullptr, *gval = nullptr, *gtmp = nullptr;
   uint8_t* gprom = nullptr;
@@ -86,6 +90,7 @@ struct gmg_ctx {
   bool force_simple_gs = false;
   int gs_max_tasks = 0;
   bool no_ws = false;
+  bool ghost_batched = false;  // one launch per ghost batch instead of the persistent sweep
   int ws_ctas_per_sm = 4;
   bool prof = false;
   int prof_mask = 0;   // bit k: time kernel class k
@@ -143,7 +148,8 @@ int upload(gmg_ctx* ctx, T** p, const T* host, int64_t count) {
 void free_level(DevLevel& l) {
   void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
-                  l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.cinv, l.cpart};  // ticket lives in progress
+                  l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.cinv, l.cpart,
+                  l.dep_off, l.dep, l.gctr};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -276,7 +282,7 @@ inline int64_t flat_to_pos(const Geom& g, int64_t flat) {
 GhostArgs ghost_args(const DevLevel& l) {
   GhostArgs a;
   a.g = l.g;
-  a.ng = l.ng;
+  a.ng = l.nslots;
   a.node = l.gnode;
   a.base = l.gbase;
   a.w = l.gw;
@@ -362,12 +368,20 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
 }
 
 int op_ghost_sweep(gmg_ctx* ctx, DevLevel& l) {
+  if (l.ng == 0) return 0;
   Scope s(ctx, 1);
   GhostArgs a = ghost_args(l);
-  for (size_t b = 0; b + 1 < l.batch_off.size(); ++b) {
-    launch_ghost_batch(a, l.u, l.batch_off[b], l.batch_off[b + 1], ctx->stream);
-    ctx->launches++;
+  const int nb = (int)l.batch_off.size() - 1;
+  if (ctx->ghost_batched) {  // one launch per batch (reference path for experiments)
+    for (int b = 0; b < nb; ++b) {
+      launch_ghost_batch(a, l.u, l.batch_off[b], l.batch_off[b + 1], ctx->stream);
+      ctx->launches++;
+    }
+    return 0;
   }
+  GMG_CHECK(ctx, cudaMemsetAsync(l.gctr, 0, sizeof(int) * (size_t)(l.nslots + 1), ctx->stream));
+  launch_ghost_persistent(a, l.u, l.dep_off, l.dep, l.gctr, ctx->sms, ctx->stream);
+  ctx->launches++;
   return 0;
 }
 
@@ -514,6 +528,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_MAX_TASKS")) ctx->gs_max_tasks = atoi(e);
   if (const char* e = getenv("GMG_NO_WS")) ctx->no_ws = e[0] == '1';
   if (const char* e = getenv("GMG_NO_GRAPH")) ctx->use_graph = e[0] != '1';
+  if (const char* e = getenv("GMG_GHOST_BATCHED")) ctx->ghost_batched = e[0] == '1';
   configure_kernels();
   if (cudaMalloc(&ctx->dmax, 8 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost(&ctx->hmax, 8 * sizeof(unsigned long long)) != cudaSuccess) {
@@ -584,45 +599,89 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   GMG_CHECK(ctx, cudaMemset(l.rI, 0, sizeof(double) * alloc));
   GMG_CHECK(ctx, cudaMemset(l.rE, 0, sizeof(double) * alloc));
 
-  // ghosts -> slot order (stable by batch)
+  // ghosts -> slot order: stable by sweep batch, each batch padded to a
+  // multiple of 32 slots so a warp's chunk never straddles two batches
   l.ng = ng;
   if (ng > 0) {
     int32_t maxb = 0;
     for (int64_t i = 0; i < ng; ++i) maxb = std::max(maxb, ghost_batch[i]);
-    std::vector<int64_t> cnt(maxb + 2, 0);
-    for (int64_t i = 0; i < ng; ++i) cnt[ghost_batch[i] + 1]++;
-    for (int b = 0; b <= maxb; ++b) cnt[b + 1] += cnt[b];
-    l.batch_off.assign(cnt.begin(), cnt.end());
-    std::vector<int32_t> s2l(ng), l2s(ng);
-    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    std::vector<int64_t> cnt(maxb + 1, 0);
+    for (int64_t i = 0; i < ng; ++i) cnt[ghost_batch[i]]++;
+    l.batch_off.assign(maxb + 2, 0);
+    for (int b = 0; b <= maxb; ++b) l.batch_off[b + 1] = l.batch_off[b] + (cnt[b] + 31) / 32 * 32;
+    const int64_t ns = l.batch_off[maxb + 1];
+    l.nslots = ns;
+    std::vector<int32_t> s2l(ns, -1), l2s(ng);
+    std::vector<int64_t> fill(l.batch_off.begin(), l.batch_off.end() - 1);
     for (int64_t i = 0; i < ng; ++i) {
-      int64_t s = fill[ghost_batch[i]]++;
+      const int64_t s = fill[ghost_batch[i]]++;
       s2l[s] = (int32_t)i;
       l2s[i] = (int32_t)s;
     }
-    std::vector<int64_t> node(ng), base(ng);
-    std::vector<double> w((size_t)m * ng), dt(ng);
-    std::vector<uint8_t> pr(ng);
+    std::vector<int64_t> node(ns, -1), base(ns, OFF);
+    std::vector<double> w((size_t)m * ns, 0.0), dt(ns, 0.0);
+    std::vector<uint8_t> pr(ns, 0);
     const int64_t st[3] = {l.g.s0, l.g.s1, l.g.s2};
-    for (int64_t s = 0; s < ng; ++s) {
+    for (int64_t s = 0; s < ns; ++s) {
       const int64_t i = s2l[s];
+      if (i < 0) continue;
       node[s] = flat_to_pos(l.g, ghost_idx[i]);
       int64_t b = OFF;
       for (int k = 0; k < d; ++k) b += ghost_low[i * d + k] * st[k];
       base[s] = b;
-      for (int j = 0; j < m; ++j) w[(size_t)j * ng + s] = ghost_w[i * m + j];
+      for (int j = 0; j < m; ++j) w[(size_t)j * ns + s] = ghost_w[i * m + j];
       dt[s] = ghost_dtau[i];
       pr[s] = ghost_promoted[i];
     }
-    if (upload(ctx, &l.gnode, node.data(), ng) || upload(ctx, &l.gbase, base.data(), ng) ||
-        upload(ctx, &l.gw, w.data(), (int64_t)m * ng) || upload(ctx, &l.gdtau, dt.data(), ng) ||
-        upload(ctx, &l.gprom, pr.data(), ng) || upload(ctx, &l.slot2lex, s2l.data(), ng) ||
-        upload(ctx, &l.lex2slot, l2s.data(), ng) || dalloc(ctx, &l.gval, ng) ||
-        dalloc(ctx, &l.gtmp, ng))
+    // dependency lists in slot space: ghost t waits for every earlier ghost
+    // s it reads or that reads it (nonzero weight) -- the edges of
+    // transfer.ghost_dag_levels, whose batches order the slots
+    std::vector<int32_t> lexmap;
+    {
+      int64_t nflat = 1;
+      for (int k = 0; k < d; ++k) nflat *= (N + 1);
+      lexmap.assign((size_t)nflat, -1);
+    }
+    for (int64_t i = 0; i < ng; ++i) lexmap[ghost_idx[i]] = (int32_t)i;
+    std::vector<int64_t> pairs;  // (later slot << 32) | earlier slot
+    pairs.reserve((size_t)ng * 4);
+    const int64_t n1 = N + 1;
+    for (int64_t i = 0; i < ng; ++i) {
+      for (int j = 0; j < m; ++j) {
+        if (ghost_w[i * m + j] == 0.0) continue;
+        int64_t flat = 0;
+        for (int k = 0; k < d; ++k) {
+          const int o = d == 3 ? (k == 0 ? j / 9 : k == 1 ? (j / 3) % 3 : j % 3) : (k == 0 ? j / 3 : j % 3);
+          flat = flat * n1 + ghost_low[i * d + k] + o;
+        }
+        const int32_t jg = lexmap[flat];
+        if (jg < 0 || jg == i) continue;
+        const int64_t a = l2s[std::min<int64_t>(i, jg)], b = l2s[std::max<int64_t>(i, jg)];
+        pairs.push_back((b << 32) | a);
+      }
+    }
+    std::sort(pairs.begin(), pairs.end());
+    pairs.erase(std::unique(pairs.begin(), pairs.end()), pairs.end());
+    std::vector<int32_t> doff((size_t)ns + 1, 0), dep(pairs.size());
+    for (size_t k = 0; k < pairs.size(); ++k) {
+      doff[(size_t)(pairs[k] >> 32) + 1]++;
+      dep[k] = (int32_t)(pairs[k] & 0xffffffff);
+    }
+    for (int64_t t = 0; t < ns; ++t) doff[t + 1] += doff[t];
+    lexmap.clear();
+    lexmap.shrink_to_fit();
+    if (dep.empty()) dep.push_back(0);
+    if (upload(ctx, &l.gnode, node.data(), ns) || upload(ctx, &l.gbase, base.data(), ns) ||
+        upload(ctx, &l.gw, w.data(), (int64_t)m * ns) || upload(ctx, &l.gdtau, dt.data(), ns) ||
+        upload(ctx, &l.gprom, pr.data(), ns) || upload(ctx, &l.slot2lex, s2l.data(), ns) ||
+        upload(ctx, &l.lex2slot, l2s.data(), ng) || dalloc(ctx, &l.gval, ns) ||
+        dalloc(ctx, &l.gtmp, std::max(ns, ng)) || upload(ctx, &l.dep_off, doff.data(), ns + 1) ||
+        upload(ctx, &l.dep, dep.data(), (int64_t)dep.size()) || dalloc(ctx, &l.gctr, ns + 1))
       return -1;
-    GMG_CHECK(ctx, cudaMemset(l.gval, 0, sizeof(double) * ng));
+    GMG_CHECK(ctx, cudaMemset(l.gval, 0, sizeof(double) * ns));
   } else {
     l.batch_off.assign(1, 0);
+    l.nslots = 0;
   }
 
   // band
@@ -758,7 +817,7 @@ int gmg_set_vector(gmg_ctx* ctx, int li, int which, const double* host) {
   if (which == GMG_G) {
     if (l.ng == 0) return 0;
     GMG_CHECK(ctx, cudaMemcpyAsync(l.gtmp, host, sizeof(double) * l.ng, cudaMemcpyHostToDevice, ctx->stream));
-    launch_permute(l.gtmp, l.slot2lex, l.ng, l.gval, ctx->stream);
+    launch_permute(l.gtmp, l.slot2lex, l.nslots, l.gval, ctx->stream);
     ctx->launches++;
     GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
     return 0;

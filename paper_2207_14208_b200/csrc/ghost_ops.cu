@@ -5,6 +5,8 @@
 // transfer.ghost_dag_levels), lexicographic inside a batch.  Weights are
 // stored [m][ng] so a warp reading one stencil entry for 32 ghosts is one
 // coalesced load.
+#include <algorithm>
+
 #include "gmg_kernels.cuh"
 
 namespace gmg {
@@ -27,6 +29,8 @@ __global__ void __launch_bounds__(256) ghost_batch_kernel(GhostArgs a, double* _
   constexpr int M = D == 3 ? 27 : 9;
   const int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= hi) return;
+  const int64_t node = a.node[s];
+  if (node < 0) return;
   const int64_t base = a.base[s];
   double x[M], y[M];
 #pragma unroll
@@ -35,9 +39,72 @@ __global__ void __launch_bounds__(256) ghost_batch_kernel(GhostArgs a, double* _
     y[j] = u[base + block_offset<D>(a.g, j)];
   }
   const double dot = blas_ddot<M>(x, y);
-  const int64_t node = a.node[s];
   u[node] = u[node] + a.dtau[s] * (a.gval[s] - dot);
 }
+
+__device__ __forceinline__ int ld_acquire_i(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_i(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// The whole ghost sweep in one launch, ordered by the sweep DAG instead of
+// batch barriers: warps claim 32-slot chunks in slot order (batch, lex); a
+// ghost waits (acquire) on the done flags of exactly the earlier ghosts it
+// reads or that read it, relaxes, stores, and releases its own flag.  Every
+// dependency lies in an earlier batch, hence an earlier chunk already held by
+// a running warp, so the sweep cannot deadlock, and each ghost sees the same
+// values as in the reference's lexicographic loop.  flags[nslots] is the
+// chunk cursor; all flags are zeroed before the launch.
+template <int D>
+__global__ void __launch_bounds__(256) ghost_persistent_kernel(GhostArgs a, double* __restrict__ u,
+                                                               const int32_t* __restrict__ dep_off,
+                                                               const int32_t* __restrict__ dep, int* flags) {
+  constexpr int M = D == 3 ? 27 : 9;
+  const int lane = threadIdx.x & 31;
+  const int64_t nchunks = a.ng / 32;
+  for (;;) {
+    int chunk = 0;
+    if (lane == 0) chunk = atomicAdd(&flags[a.ng], 1);
+    chunk = __shfl_sync(0xffffffffu, chunk, 0);
+    if (chunk >= nchunks) return;
+    const int64_t s = (int64_t)chunk * 32 + lane;
+    const int64_t node = a.node[s];
+    if (node >= 0) {
+      const int64_t base = a.base[s];
+      double x[M], y[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) x[j] = __ldg(a.w + (int64_t)j * a.ng + s);
+      const double gv = a.gval[s], dt = a.dtau[s];
+      const int d1 = dep_off[s + 1];
+      for (int k = dep_off[s]; k < d1; ++k) {
+        const int* f = flags + dep[k];
+        while (ld_acquire_i(f) == 0) {
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < M; ++j) y[j] = __ldcg(u + base + block_offset<D>(a.g, j));
+      const double dot = blas_ddot<M>(x, y);
+      __stcg(u + node, __ldcg(u + node) + dt * (gv - dot));
+      st_release_i(flags + s, 1);
+    }
+  }
+}
+
+void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_off, const int32_t* dep, int* flags,
+                             int sms, cudaStream_t st) {
+  const int64_t warps = a.ng / 32;
+  int blocks = (int)std::min<int64_t>((warps + 7) / 8, (int64_t)sms * 8);
+  if (blocks < 1) blocks = 1;
+  if (a.g.d == 3)
+    ghost_persistent_kernel<3><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, flags);
+  else
+    ghost_persistent_kernel<2><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, flags);
+}
+
 
 void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st) {
   if (hi <= lo) return;
@@ -73,7 +140,7 @@ __global__ void __launch_bounds__(256) residual_ghost_kernel(GhostArgs a, const 
   constexpr int M = D == 3 ? 27 : 9;
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double am = 0.0;
-  if (s < a.ng) {
+  if (s < a.ng && a.node[s] >= 0) {
     const int64_t base = a.base[s];
     double p[M];
 #pragma unroll
@@ -123,7 +190,7 @@ __global__ void __launch_bounds__(256) restrict_ghost_kernel(Geom gf, const uint
   constexpr int M = D == 3 ? 27 : 9;
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= c.ng) return;
-  if (c.promoted[s]) {
+  if (c.promoted[s] || c.node[s] < 0) {
     gval_c[s] = 0.0;
     return;
   }

@@ -24,7 +24,7 @@ struct GsArgs {
 // Ghost rows of one level, stored in sweep-slot order (batch, then lex).
 struct GhostArgs {
   Geom g;
-  int64_t ng;
+  int64_t ng;            // slots (ghosts padded per batch); node < 0 marks an empty slot
   const int64_t* node;   // ghost node
   const int64_t* base;   // flat index of the 3^d block's low corner
   const double* w;       // [m][ng] row weights, m = 3^d
@@ -55,6 +55,8 @@ size_t gs_ws_smem();
 void configure_gs_kernels();  // set max dynamic shared memory of the GS / GEMV kernels
 
 void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st);
+void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_off, const int32_t* dep, int* flags,
+                             int sms, cudaStream_t st);
 void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,
                            unsigned long long* maxbits, cudaStream_t st);
 void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,

@@ -307,11 +307,11 @@ void launch_scatter(const int64_t* idx, int64_t n, const double* x, double* e, c
   scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(idx, n, x, e);
 }
 
-// dst[i] = src[perm[i]]
+// dst[i] = src[perm[i]] (0 where perm[i] < 0)
 __global__ void permute_kernel(const double* __restrict__ src, const int32_t* __restrict__ perm, int64_t n,
                                double* __restrict__ dst) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = src[perm[i]];
+  if (i < n) dst[i] = perm[i] >= 0 ? src[perm[i]] : 0.0;
 }
 
 void launch_permute(const double* src, const int32_t* perm, int64_t n, double* dst, cudaStream_t st) {
