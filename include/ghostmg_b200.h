@@ -128,6 +128,12 @@ int gmg_synchronize(gmg_ctx *ctx);
 
 /* Kernels launched by this context so far. */
 int64_t gmg_launch_count(const gmg_ctx *ctx);
+/* Diagnostics: with GMG_GS_TRACE=1 in the environment the Gauss-Seidel
+ * kernel records 16 int64 per task (start/end globaltimer ns, SM id, compute
+ * warp cycles waiting for data / in total, loader waits and idle polls, see
+ * tools/gs_trace.py).  Copies up to `cap` values of the last sweep on
+ * `level`; returns the count (0 if not traced). */
+int64_t gmg_debug_gs_trace(gmg_ctx *ctx, int level, long long *host, int64_t cap);
 /* Device bytes held by the context. */
 int64_t gmg_device_bytes(const gmg_ctx *ctx);
 

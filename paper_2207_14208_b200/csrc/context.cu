@@ -34,6 +34,7 @@ struct DevLevel {
   int32_t* dep_off = nullptr;  // [nslots+1] CSR: slots each slot must wait for
   int32_t* dep = nullptr;
   int* gctr = nullptr;         // [nslots] done flags + chunk cursor
+  long long* trace = nullptr;  // GS task timeline (diagnostics)
   int64_t *gnode = nullptr, *gbase = nullptr;
   double *gw = nullptr, *gdtau = nullptr, *gval = nullptr, *gtmp = nullptr;
   uint8_t* gprom = nullptr;
@@ -50,9 +51,11 @@ struct DevLevel {
   int2* tasks = nullptr;
   int ntasks = 0, B1 = 1, Bn = 1, C = 1;
   uint32_t* imask = nullptr;  // streaming GS: internal bitmask per (line, chunk)
+  uint32_t* imask2 = nullptr; // diagonal GS (3-D): masks per (plane, block, pseudo-line)
   int Cm = 4;                 // imask row stride (C rounded up to 4)
   bool stream_gs = false;
   bool ws_gs = false;         // warp-specialised TMA kernel
+  bool diag_gs = false;       // lane-diagonal ring kernel (production, N >= 64)
   WsMaps maps;                // its tensor maps (u, f, imask)
   int *progress = nullptr, *ticket = nullptr;
   // coarsest direct solve
@@ -90,7 +93,10 @@ struct gmg_ctx {
   bool force_simple_gs = false;
   int gs_max_tasks = 0;
   bool no_ws = false;
-  bool ghost_batched = false;  // one launch per ghost batch instead of the persistent sweep
+  bool ghost_batched = false;
+  bool gs_trace = false;       // record the GS task timeline (GMG_GS_TRACE=1)
+  bool gs_ws = false;          // use the older TMA-ring GS kernel (GMG_GS_WS=1)
+  int gs_variant = 0;          // GS implementation variant (GMG_GS_VARIANT, experiments)  // one launch per ghost batch instead of the persistent sweep
   int ws_ctas_per_sm = 4;
   bool prof = false;
   int prof_mask = 0;   // bit k: time kernel class k
@@ -148,8 +154,8 @@ int upload(gmg_ctx* ctx, T** p, const T* host, int64_t count) {
 void free_level(DevLevel& l) {
   void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
-                  l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.cinv, l.cpart,
-                  l.dep_off, l.dep, l.gctr};  // ticket lives in progress
+                  l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
+                  l.dep_off, l.dep, l.gctr, l.trace};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -245,6 +251,9 @@ Geom make_geom(int d, int64_t N, double reaction) {
   g.N = N;
   g.n = N + 1;
   g.P = ((N + OFF + 1) + 3) / 4 * 4;  // >= n + OFF, multiple of 4 doubles
+  // the Gauss-Seidel kernels move whole 32-column chunks (columns 1+32c ..
+  // 32+32c): keep the last chunk inside its row
+  g.P = std::max<int64_t>(g.P, 32 * ((N - 1 + 31) / 32) + 4);
   if (d == 3) {
     g.rows = g.n * g.n;
     g.s0 = g.n * g.P;
@@ -321,6 +330,19 @@ EncodeTiledFn encode_fn() {
 }
 
 // 2-D tiled tensor map over `rows` rows of `cols` elements (row pitch in bytes)
+bool make_map3(CUtensorMap* m, void* base, uint64_t cols, uint64_t rows, uint64_t planes, uint32_t box0,
+               uint32_t box1) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {cols, rows, planes};
+  cuuint64_t strides[2] = {cols * 8, cols * rows * 8};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap* m, CUtensorMapDataType t, void* base, uint64_t cols, uint64_t rows,
               uint64_t pitch_bytes, uint32_t box0, uint32_t box1) {
   EncodeTiledFn fn = encode_fn();
@@ -341,7 +363,7 @@ int gs_grid(const DevLevel& l) {
 // ---- operations ------------------------------------------------------------
 int op_gs(gmg_ctx* ctx, DevLevel& l) {
   Scope s(ctx, 0);
-  GMG_CHECK(ctx, cudaMemsetAsync(l.progress, 0, sizeof(int) * (size_t)(l.C * l.Bn + 1), ctx->stream));
+  GMG_CHECK(ctx, cudaMemsetAsync(l.progress, 0, sizeof(int) * (size_t)(4 * l.C * l.Bn + 4), ctx->stream));
   GsArgs a;
   a.g = l.g;
   a.labels = l.labels;
@@ -356,8 +378,17 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
   a.C = l.C;
   a.imask = l.imask;
   a.Cm = l.Cm;
+  a.trace = nullptr;
+  a.variant = ctx->gs_variant;
+  if (ctx->gs_trace && (l.ws_gs || l.diag_gs)) {
+    if (!l.trace && dalloc(ctx, &l.trace, (int64_t)l.ntasks * 16)) return -1;
+    GMG_CHECK(ctx, cudaMemsetAsync(l.trace, 0, sizeof(long long) * (size_t)l.ntasks * 16, ctx->stream));
+    a.trace = l.trace;
+  }
   if (ctx->gs_max_tasks > 0) a.ntasks = std::min(a.ntasks, ctx->gs_max_tasks);  // timing experiments only
-  if (l.ws_gs)
+  if (l.diag_gs)
+    launch_gs_diag(a, l.maps, std::min(a.ntasks, ctx->ws_ctas_per_sm * ctx->sms), ctx->stream);
+  else if (l.ws_gs)
     launch_gs_ws(a, l.maps, std::min(a.ntasks, ctx->ws_ctas_per_sm * ctx->sms), ctx->stream);
   else if (l.stream_gs)
     launch_gs_stream(a, std::min(l.ntasks, 4 * ctx->sms), 1, ctx->stream);
@@ -529,6 +560,9 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_NO_WS")) ctx->no_ws = e[0] == '1';
   if (const char* e = getenv("GMG_NO_GRAPH")) ctx->use_graph = e[0] != '1';
   if (const char* e = getenv("GMG_GHOST_BATCHED")) ctx->ghost_batched = e[0] == '1';
+  if (const char* e = getenv("GMG_GS_TRACE")) ctx->gs_trace = e[0] == '1';
+  if (const char* e = getenv("GMG_GS_WS")) ctx->gs_ws = e[0] == '1';
+  if (const char* e = getenv("GMG_GS_VARIANT")) ctx->gs_variant = atoi(e);
   configure_kernels();
   if (cudaMalloc(&ctx->dmax, 8 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost(&ctx->hmax, 8 * sizeof(unsigned long long)) != cudaSuccess) {
@@ -705,8 +739,9 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   l.C = (int)((N - 1 + 31) / 32);
   l.stream_gs = N >= 32 && !ctx->force_simple_gs;
   l.ws_gs = N >= 64 && !ctx->force_simple_gs && !ctx->no_ws && encode_fn() != nullptr;
+  l.diag_gs = l.ws_gs && !ctx->gs_ws;
   if (d == 3) {
-    l.B1 = l.stream_gs ? 16 : 8;
+    l.B1 = l.diag_gs ? 14 : (l.stream_gs ? 16 : 8);
     l.Bn = (int)((N - 1 + l.B1 - 1) / l.B1);
   } else {
     l.B1 = 1;
@@ -731,6 +766,32 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
           !make_map(&l.maps.m, CU_TENSOR_MAP_DATA_TYPE_UINT32, l.imask, (uint64_t)l.Cm, (uint64_t)lines,
                     (uint64_t)l.Cm * 4, 4, 8))
         return fail(ctx, "cuTensorMapEncodeTiled failed");
+      if (l.diag_gs) {
+        const bool ok = d == 3 ? make_map3(&l.maps.ust, l.u, P, (uint64_t)n, (uint64_t)n, 32, 7)
+                               : make_map(&l.maps.ust, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, l.u, P, (uint64_t)n, P * 8,
+                                          32, 8);
+        if (!ok) return fail(ctx, "store tensor map failed");
+      }
+      if (l.diag_gs && d == 3) {
+        // pseudo-line r of block b in plane p (1..N-1): row rowbase-1+r for 1 <= r <= Rb, else zero
+        const int PLn = 16;
+        const int64_t rows2 = (N - 1) * (int64_t)l.Bn * PLn;
+        std::vector<uint32_t> im2((size_t)(rows2 * l.Cm), 0u);
+        for (int64_t p = 1; p <= N - 1; ++p)
+          for (int b = 0; b < l.Bn; ++b) {
+            const int64_t rowbase = 1 + (int64_t)l.B1 * b;
+            const int64_t Rb = std::min<int64_t>(l.B1, N - 1 - l.B1 * (int64_t)b);
+            for (int64_t r = 1; r <= Rb; ++r) {
+              const int64_t src = (p * n + rowbase - 1 + r) * l.Cm;
+              const int64_t dst = (((p - 1) * l.Bn + b) * PLn + r) * l.Cm;
+              std::memcpy(&im2[(size_t)dst], &im[(size_t)src], sizeof(uint32_t) * l.Cm);
+            }
+          }
+        if (upload(ctx, &l.imask2, im2.data(), rows2 * l.Cm) ||
+            !make_map(&l.maps.m2, CU_TENSOR_MAP_DATA_TYPE_UINT32, l.imask2, (uint64_t)l.Cm, (uint64_t)rows2,
+                      (uint64_t)l.Cm * 4, 4, 8))
+          return fail(ctx, "block mask upload / tensor map failed");
+      }
     }
   }
   std::vector<int2> tasks;
@@ -740,9 +801,11 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
       if (b >= 0 && b < l.Bn) tasks.push_back(make_int2(c, b));
     }
   l.ntasks = (int)tasks.size();
-  if (upload(ctx, &l.tasks, tasks.data(), l.ntasks) || dalloc(ctx, &l.progress, l.C * l.Bn + 1))
+  // progress words: 16 B per task (the TMA-store path writes them with bulk copies);
+  // the older kernels use the first C * Bn ints
+  if (upload(ctx, &l.tasks, tasks.data(), l.ntasks) || dalloc(ctx, &l.progress, 4 * l.C * l.Bn + 4))
     return -1;
-  l.ticket = l.progress + l.C * l.Bn;
+  l.ticket = l.progress + 4 * l.C * l.Bn;
 
   // coarsest direct-solve ordering: internal then ghost (ref operators.py:180)
   if (li == ctx->nlevels - 1) {
@@ -991,6 +1054,17 @@ int gmg_synchronize(gmg_ctx* ctx) {
 }
 
 int64_t gmg_launch_count(const gmg_ctx* ctx) { return ctx->launches; }
+
+int64_t gmg_debug_gs_trace(gmg_ctx* ctx, int li, long long* host, int64_t cap) {
+  if (li < 0 || li >= ctx->nlevels) return fail(ctx, "bad level");
+  DevLevel& l = ctx->L[li];
+  if (!l.trace) return 0;
+  const int64_t n = std::min<int64_t>(cap, (int64_t)l.ntasks * 16);
+  cudaSetDevice(ctx->device);
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  GMG_CHECK(ctx, cudaMemcpy(host, l.trace, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+  return n;
+}
 int64_t gmg_device_bytes(const gmg_ctx* ctx) { return ctx->bytes; }
 
 int gmg_profile(gmg_ctx* ctx, int mask) {

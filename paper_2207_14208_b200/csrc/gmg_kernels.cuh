@@ -19,6 +19,8 @@ struct GsArgs {
   int B1, Bn, C;
   const uint32_t* imask;  // per (line, chunk) bitmask of internal nodes, row stride Cm
   int Cm;                 // C rounded up to a multiple of 4
+  long long* trace;       // diagnostics: [ntasks][16] timeline per task, or null
+  int variant;            // diagnostics: GS implementation variant (GMG_GS_VARIANT)
 };
 
 // Ghost rows of one level, stored in sweep-slot order (batch, then lex).
@@ -49,9 +51,13 @@ size_t gs_stream_smem_per_warp();
 // TMA tensor maps of one level for the warp-specialised GS kernel
 struct WsMaps {
   CUtensorMap u, f, m;
+  CUtensorMap m2;  // 3-D: internal-node masks per (plane, block, pseudo-line), zero on halo lines
+  CUtensorMap ust; // u as (plane, row, col) with 7-row boxes (3-D) / (row, col) 8-row boxes (2-D), TMA stores
 };
 void launch_gs_ws(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st);
 size_t gs_ws_smem();
+void launch_gs_diag(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st);
+size_t gs_diag_smem();
 void configure_gs_kernels();  // set max dynamic shared memory of the GS / GEMV kernels
 
 void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st);

@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(32) gs_stream_kernel(GsArgs a) {
 size_t gs_stream_smem_per_warp() { return sizeof(WarpRing); }
 
 void configure_gs_ws();
+void configure_gs_diag();
 void configure_dense_gemv();
 
 void configure_gs_kernels() {
@@ -257,6 +258,7 @@ void configure_gs_kernels() {
   cudaFuncSetAttribute(gs_stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(gs_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   configure_gs_ws();
+  configure_gs_diag();
   configure_dense_gemv();
 }
 

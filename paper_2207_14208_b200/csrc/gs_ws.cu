@@ -116,6 +116,11 @@ __device__ __forceinline__ int ld_acquire_cta(const int* p) {
 __device__ __forceinline__ void st_release_cta(int* p, int v) {
   asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(sa(p)), "r"(v) : "memory");
 }
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
 }  // namespace
@@ -159,6 +164,7 @@ __global__ void __launch_bounds__(64, 1) gs_ws_kernel(GsArgs a, const __grid_con
       return L + 1;
     };
     const int last = nLines + 30;  // last consumer step
+    long long* const tr = a.trace ? a.trace + (int64_t)tid * 16 : nullptr;
 
     if (warp == 1) {
       // =============================== producer ===========================
@@ -171,6 +177,7 @@ __global__ void __launch_bounds__(64, 1) gs_ws_kernel(GsArgs a, const __grid_con
         const int nwb = nLines / G;           // write-back batches (nLines multiple of G)
         const int ux = k0 + (int)OFF - 2, fx = k0 + (int)OFF, mx = c & ~3;
         int q = 0, w = 0, published = 0, l2q = L2AHEAD / G;
+        long long waitL = 0, waitU = 0, idle = 0;
         while (q < nbatches || published < nLines) {
           const int cs = ld_acquire_cta(&S.cons_step);
           bool did = false;
@@ -215,12 +222,17 @@ __global__ void __launch_bounds__(64, 1) gs_ws_kernel(GsArgs a, const __grid_con
             }
             if (ok) {
               const int lastreal = min(L0 + G, nLines) - 1;
-              if (lprog && lastreal >= 0)
+              if (lprog && lastreal >= 0 && seenL < lastreal + 1) {
+                const long long c0 = tr ? clock64() : 0;
                 while (seenL < lastreal + 1) seenL = ld_acquire(lprog);
+                if (tr) waitL += clock64() - c0;
+              }
               const bool pstart = DIM == 3 && L0 >= 0 && L0 < nLines && (L0 % R) == 0;
               if (uprog && pstart) {
                 const int need = (L0 / R + 1) * 16;
+                const long long c0 = tr ? clock64() : 0;
                 while (seenU < need) seenU = ld_acquire(uprog);
+                if (tr) waitU += clock64() - c0;
               }
               fence_async_global();
               const unsigned bar = sa(&S.full[q % NB]);
@@ -247,9 +259,17 @@ __global__ void __launch_bounds__(64, 1) gs_ws_kernel(GsArgs a, const __grid_con
               did = true;
             }
           }
-          if (!did) __nanosleep(32);
+          if (!did) {
+            ++idle;
+            __nanosleep(32);
+          }
         }
         bulk_wait<0>();
+        if (tr) {
+          tr[5] = waitL;
+          tr[6] = waitU;
+          tr[7] = idle;
+        }
       }
       __syncwarp();
     } else {
@@ -262,12 +282,24 @@ __global__ void __launch_bounds__(64, 1) gs_ws_kernel(GsArgs a, const __grid_con
       const bool kval = k0 + lane <= N - 1;
       const int mword = c & 3;
       int ready = 0;
+      long long cwait = 0;
+      const long long cstart = clock64();
+      if (tr && lane == 0) {
+        tr[0] = gtimer();
+        unsigned sm;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+        tr[2] = sm;
+      }
       auto wait_lines = [&](int t) {
         // lines up to t + R must be resident: batch of Lr = t + 2R
         while (ready * G <= min(t + 2 * R, uEnd + R - 1)) {
           const unsigned bar = sa(&S.full[ready % NB]);
           const unsigned par = (unsigned)((ready / NB) & 1);
-          while (!mbar_try_wait(bar, par)) {
+          if (!mbar_try_wait(bar, par)) {
+            const long long c0 = tr ? clock64() : 0;
+            while (!mbar_try_wait(bar, par)) {
+            }
+            if (tr) cwait += clock64() - c0;
           }
           ++ready;
         }
@@ -336,6 +368,11 @@ __global__ void __launch_bounds__(64, 1) gs_ws_kernel(GsArgs a, const __grid_con
           if (lane == 0) st_release_cta(&S.cons_step, t);
         }
         __syncwarp();
+      }
+      if (tr && lane == 0) {
+        tr[1] = gtimer();
+        tr[3] = cwait;
+        tr[4] = clock64() - cstart;
       }
     }
     __syncthreads();
