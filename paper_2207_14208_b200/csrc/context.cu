@@ -96,7 +96,8 @@ struct gmg_ctx {
   bool ghost_batched = false;
   bool gs_trace = false;       // record the GS task timeline (GMG_GS_TRACE=1)
   bool gs_ws = false;          // use the older TMA-ring GS kernel (GMG_GS_WS=1)
-  int gs_variant = 0;          // GS implementation variant (GMG_GS_VARIANT, experiments)  // one launch per ghost batch instead of the persistent sweep
+  int gs_variant = 0;          // GS implementation variant (GMG_GS_VARIANT, experiments)
+  int gs_sleep[4] = {500, 500, 20, 200};  // GS loader / writer back-off (ns), GMG_GS_SLEEP=u,f,h,w  // one launch per ghost batch instead of the persistent sweep
   int ws_ctas_per_sm = 4;
   bool prof = false;
   int prof_mask = 0;   // bit k: time kernel class k
@@ -380,6 +381,7 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
   a.Cm = l.Cm;
   a.trace = nullptr;
   a.variant = ctx->gs_variant;
+  for (int i = 0; i < 4; ++i) a.sleep_ns[i] = ctx->gs_sleep[i];
   if (ctx->gs_trace && (l.ws_gs || l.diag_gs)) {
     if (!l.trace && dalloc(ctx, &l.trace, (int64_t)l.ntasks * 16)) return -1;
     GMG_CHECK(ctx, cudaMemsetAsync(l.trace, 0, sizeof(long long) * (size_t)l.ntasks * 16, ctx->stream));
@@ -563,6 +565,8 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_TRACE")) ctx->gs_trace = e[0] == '1';
   if (const char* e = getenv("GMG_GS_WS")) ctx->gs_ws = e[0] == '1';
   if (const char* e = getenv("GMG_GS_VARIANT")) ctx->gs_variant = atoi(e);
+  if (const char* e = getenv("GMG_GS_SLEEP"))
+    sscanf(e, "%d,%d,%d,%d", &ctx->gs_sleep[0], &ctx->gs_sleep[1], &ctx->gs_sleep[2], &ctx->gs_sleep[3]);
   configure_kernels();
   if (cudaMalloc(&ctx->dmax, 8 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMallocHost(&ctx->hmax, 8 * sizeof(unsigned long long)) != cudaSuccess) {

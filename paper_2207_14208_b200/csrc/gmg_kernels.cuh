@@ -21,6 +21,7 @@ struct GsArgs {
   int Cm;                 // C rounded up to a multiple of 4
   long long* trace;       // diagnostics: [ntasks][16] timeline per task, or null
   int variant;            // diagnostics: GS implementation variant (GMG_GS_VARIANT)
+  int sleep_ns[4];        // back-off of the u / f / halo loaders and the writer when idle
 };
 
 // Ghost rows of one level, stored in sweep-slot order (batch, then lex).

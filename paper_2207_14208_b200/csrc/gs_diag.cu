@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         tr[1] = gtimer();
         tr[3] = cwU + cwF + cwH;
         tr[4] = clock64() - cstart;
-        tr[8] = cwF + cwU * 0;
+        tr[8] = cwU + cwF;  // u + f waits (tr[3] - tr[8]: halo waits)
         (void)cwH;
       }
     } else if (warp == 1) {
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         if (ok && old >= 0) ok = ld_flag(&S.wdone) >= min(old + 1, nLines);
         if (!ok) {
           ++bidle;
-          __nanosleep(20);
+          __nanosleep(a.sleep_ns[0]);
           continue;
         }
         const long long c0 = tr ? clock64() : 0;
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         const int cs = ld_flag(&S.cons);
         // slot of line L held line L - RFL, read by lane 31 up to step L - RFL + 31
         if (!(qF < NFq && cs >= 8 * qF - 32 + 7 - RFL + 30)) {
-          __nanosleep(20);
+          __nanosleep(a.sleep_ns[1]);
           continue;
         }
         const int lo = 8 * qF - 32;
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
       double hvA = 0.0, uwA = 0.0, hvB = 0.0, uwB = 0.0;
       while (hs < NHq) {
         if (hi == hs) {  // slot A empty: block until batch hs may be issued
-          while (!ready(hs, true)) __nanosleep(20);
+          while (!ready(hs, true)) __nanosleep(a.sleep_ns[2]);
           issue(hs, hvA, uwA);
           ++hi;
         }
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         }
         if (!did) {
           ++idle;
-          __nanosleep(20);
+          __nanosleep(a.sleep_ns[3]);
         }
       }
       if (lane == 0) {

@@ -123,3 +123,10 @@ if d == 3 and nt == len(tasks):
     print(f"task (0,0) step time between batches 64 and 512: {rate * 1e3:.1f} ns")
 os.makedirs("gpurun_out", exist_ok=True)
 np.savez(f"gpurun_out/gs_trace_{name}{N}_L{level}.npz", trace=tr, tasks=np.array(tasks[:nt]))
+# per-task breakdown of a few tasks (cycles per step)
+for key in [(0, 0), (1, 0), (0, 1), (C // 2, Bn // 2)]:
+    if key in {tuple(t) for t in tasks[:nt]}:
+        i = [tuple(t) for t in tasks[:nt]].index(key)
+        t = tr[i]
+        print(f"task {key}: total {t[4] / steps:.0f} cyc/step, waits: u+f {t[8] / steps:.0f}, "
+              f"halo {(t[3] - t[8]) / steps:.0f}; compute {(t[4] - t[3]) / steps:.0f}")
