@@ -134,6 +134,9 @@ int64_t gmg_launch_count(const gmg_ctx *ctx);
  * tools/gs_trace.py).  Copies up to `cap` values of the last sweep on
  * `level`; returns the count (0 if not traced). */
 int64_t gmg_debug_gs_trace(gmg_ctx *ctx, int level, long long *host, int64_t cap);
+/* Diagnostics: ghost-sweep timeline (GMG_GS_TRACE=1), 3 int64 per sweep slot
+ * (claimed, dependencies met, stored; globaltimer ns) of the last sweep. */
+int64_t gmg_debug_ghost_trace(gmg_ctx *ctx, int level, long long *host, int64_t cap);
 /* Device bytes held by the context. */
 int64_t gmg_device_bytes(const gmg_ctx *ctx);
 

@@ -49,6 +49,7 @@ SIGNATURES = {
     "gmg_synchronize": (_i, [_p]),
     "gmg_launch_count": (_i64, [_p]),
     "gmg_debug_gs_trace": (_i64, [_p, _i, _p, _i64]),
+    "gmg_debug_ghost_trace": (_i64, [_p, _i, _p, _i64]),
     "gmg_device_bytes": (_i64, [_p]),
     "gmg_profile": (_i, [_p, _i]),
     "gmg_profile_read": (_i, [_p, _i, _i, _p, _p]),
@@ -194,6 +195,12 @@ class Context:
     @property
     def launches(self):
         return int(self.lib.gmg_launch_count(self.ctx))
+
+    def ghost_trace(self, level, nslots):
+        """Ghost-sweep timeline of the last sweep on `level` (GMG_GS_TRACE=1)."""
+        out = np.zeros((nslots, 3), dtype=np.int64)
+        n = self.lib.gmg_debug_ghost_trace(self.ctx, level, out.ctypes.data, out.size)
+        return out if n else None
 
     def gs_trace(self, level, ntasks):
         """GS task timeline of the last sweep on `level` (GMG_GS_TRACE=1)."""

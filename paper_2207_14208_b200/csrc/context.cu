@@ -33,8 +33,12 @@ struct DevLevel {
   int64_t nslots = 0;  // padded slots
   int32_t* dep_off = nullptr;  // [nslots+1] CSR: slots each slot must wait for
   int32_t* dep = nullptr;
-  int* gctr = nullptr;         // [nslots] done flags + chunk cursor
+  int* gctr = nullptr;         // chunk cursor (ghost sweep)
+  uint32_t* vmask = nullptr;   // per slot: stencil entries whose value comes from an earlier ghost
+  int64_t* dbatch_off = nullptr;  // sweep batch slot offsets (device)
+  double* gpair = nullptr;     // per slot: (new value, done tag) of the running sweep
   long long* trace = nullptr;  // GS task timeline (diagnostics)
+  long long* ghtrace = nullptr;  // ghost sweep timeline (diagnostics)
   int64_t *gnode = nullptr, *gbase = nullptr;
   double *gw = nullptr, *gdtau = nullptr, *gval = nullptr, *gtmp = nullptr;
   uint8_t* gprom = nullptr;
@@ -52,6 +56,7 @@ struct DevLevel {
   int ntasks = 0, B1 = 1, Bn = 1, C = 1;
   uint32_t* imask = nullptr;  // streaming GS: internal bitmask per (line, chunk)
   uint32_t* imask2 = nullptr; // diagonal GS (3-D): masks per (plane, block, pseudo-line)
+  uint32_t* rmask = nullptr;  // restriction from the finer level: fine-label pattern per coarse node
   int Cm = 4;                 // imask row stride (C rounded up to 4)
   bool stream_gs = false;
   bool ws_gs = false;         // warp-specialised TMA kernel
@@ -97,6 +102,9 @@ struct gmg_ctx {
   bool gs_trace = false;       // record the GS task timeline (GMG_GS_TRACE=1)
   bool gs_ws = false;          // use the older TMA-ring GS kernel (GMG_GS_WS=1)
   int gs_variant = 0;          // GS implementation variant (GMG_GS_VARIANT, experiments)
+  int ghost_bps = 8;           // ghost sweep: CTAs per SM (GMG_GHOST_BPS)
+  bool ghost_levels = false;   // ghost sweep: level-synchronous kernel (GMG_GHOST_LEVELS=1; slower)
+  int ghost_backoff = 300;     // ghost sweep: poll back-off ns (GMG_GHOST_BACKOFF)
   int gs_sleep[4] = {500, 500, 20, 200};  // GS loader / writer back-off (ns), GMG_GS_SLEEP=u,f,h,w  // one launch per ghost batch instead of the persistent sweep
   int ws_ctas_per_sm = 4;
   bool prof = false;
@@ -156,7 +164,7 @@ void free_level(DevLevel& l) {
   void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
                   l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
-                  l.dep_off, l.dep, l.gctr, l.trace};  // ticket lives in progress
+                  l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -412,8 +420,21 @@ int op_ghost_sweep(gmg_ctx* ctx, DevLevel& l) {
     }
     return 0;
   }
-  GMG_CHECK(ctx, cudaMemsetAsync(l.gctr, 0, sizeof(int) * (size_t)(l.nslots + 1), ctx->stream));
-  launch_ghost_persistent(a, l.u, l.dep_off, l.dep, l.gctr, ctx->sms, ctx->stream);
+  GMG_CHECK(ctx, cudaMemsetAsync(l.gctr, 0, sizeof(int), ctx->stream));
+  GMG_CHECK(ctx, cudaMemsetAsync(l.gpair, 0, sizeof(double) * 2 * (size_t)l.nslots, ctx->stream));
+  if (ctx->ghost_levels) {
+    launch_ghost_levels(a, l.u, l.dbatch_off, nb, l.dep_off, l.dep, l.vmask, l.gpair, l.gctr, ctx->sms,
+                        ctx->stream);
+    ctx->launches++;
+    return 0;
+  }
+  long long* gtrace = nullptr;
+  if (ctx->gs_trace) {  // diagnostics: per-slot (claim, deps met, stored) globaltimer
+    if (!l.ghtrace && dalloc(ctx, &l.ghtrace, 3 * l.nslots)) return -1;
+    gtrace = l.ghtrace;
+  }
+  launch_ghost_persistent(a, l.u, l.dep_off, l.dep, l.vmask, l.gpair, l.gctr, ctx->sms, ctx->ghost_bps,
+                          ctx->ghost_backoff, gtrace, ctx->stream);
   ctx->launches++;
   return 0;
 }
@@ -456,7 +477,8 @@ int op_extend(gmg_ctx* ctx, DevLevel& l, double* x) {
 
 int op_restrict_int(gmg_ctx* ctx, DevLevel& f, DevLevel& c) {
   Scope s(ctx, 4);
-  launch_restrict_interior(f.g, f.labels, f.rI, c.g, c.labels, c.f, ctx->stream);
+  if (!c.rmask) return fail(ctx, "restriction mask missing (levels set out of order?)");
+  launch_restrict_interior(f.g, f.rI, c.g, c.rmask, c.f, ctx->stream);
   ctx->launches++;
   return 0;
 }
@@ -565,6 +587,9 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_TRACE")) ctx->gs_trace = e[0] == '1';
   if (const char* e = getenv("GMG_GS_WS")) ctx->gs_ws = e[0] == '1';
   if (const char* e = getenv("GMG_GS_VARIANT")) ctx->gs_variant = atoi(e);
+  if (const char* e = getenv("GMG_GHOST_BPS")) ctx->ghost_bps = std::max(1, atoi(e));
+  if (const char* e = getenv("GMG_GHOST_LEVELS")) ctx->ghost_levels = e[0] == '1';
+  if (const char* e = getenv("GMG_GHOST_BACKOFF")) ctx->ghost_backoff = atoi(e);
   if (const char* e = getenv("GMG_GS_SLEEP"))
     sscanf(e, "%d,%d,%d,%d", &ctx->gs_sleep[0], &ctx->gs_sleep[1], &ctx->gs_sleep[2], &ctx->gs_sleep[3]);
   configure_kernels();
@@ -681,8 +706,13 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
       lexmap.assign((size_t)nflat, -1);
     }
     for (int64_t i = 0; i < ng; ++i) lexmap[ghost_idx[i]] = (int32_t)i;
-    std::vector<int64_t> pairs;  // (later slot << 32) | earlier slot
-    pairs.reserve((size_t)ng * 4);
+    // edges (later slot b, earlier slot a, stencil index j of a in b's row, or
+    // -1 when b only has to wait for a to have read b's old value)
+    struct Edge {
+      int32_t b, a, j;
+    };
+    std::vector<Edge> edges;
+    edges.reserve((size_t)ng * 4);
     const int64_t n1 = N + 1;
     for (int64_t i = 0; i < ng; ++i) {
       for (int j = 0; j < m; ++j) {
@@ -694,16 +724,31 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
         }
         const int32_t jg = lexmap[flat];
         if (jg < 0 || jg == i) continue;
-        const int64_t a = l2s[std::min<int64_t>(i, jg)], b = l2s[std::max<int64_t>(i, jg)];
-        pairs.push_back((b << 32) | a);
+        if (jg < i)
+          edges.push_back({l2s[i], l2s[jg], j});  // i reads jg's new value
+        else
+          edges.push_back({l2s[jg], l2s[i], -1});  // jg must not change before i read it
       }
     }
-    std::sort(pairs.begin(), pairs.end());
-    pairs.erase(std::unique(pairs.begin(), pairs.end()), pairs.end());
-    std::vector<int32_t> doff((size_t)ns + 1, 0), dep(pairs.size());
-    for (size_t k = 0; k < pairs.size(); ++k) {
-      doff[(size_t)(pairs[k] >> 32) + 1]++;
-      dep[k] = (int32_t)(pairs[k] & 0xffffffff);
+    std::sort(edges.begin(), edges.end(), [](const Edge& x, const Edge& y) {
+      return x.b != y.b ? x.b < y.b : (x.a != y.a ? x.a < y.a : x.j > y.j);
+    });
+    edges.erase(std::unique(edges.begin(), edges.end(),
+                            [](const Edge& x, const Edge& y) { return x.b == y.b && x.a == y.a; }),
+                edges.end());
+    // per b: value edges in stencil order first, then wait-only edges
+    std::stable_sort(edges.begin(), edges.end(), [](const Edge& x, const Edge& y) {
+      if (x.b != y.b) return x.b < y.b;
+      const bool xv = x.j >= 0, yv = y.j >= 0;
+      if (xv != yv) return xv;
+      return xv ? x.j < y.j : false;
+    });
+    std::vector<int32_t> doff((size_t)ns + 1, 0), dep(edges.size());
+    std::vector<uint32_t> vmask((size_t)ns, 0u);
+    for (size_t k = 0; k < edges.size(); ++k) {
+      doff[(size_t)edges[k].b + 1]++;
+      dep[k] = edges[k].a;
+      if (edges[k].j >= 0) vmask[(size_t)edges[k].b] |= 1u << edges[k].j;
     }
     for (int64_t t = 0; t < ns; ++t) doff[t + 1] += doff[t];
     lexmap.clear();
@@ -714,7 +759,9 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
         upload(ctx, &l.gprom, pr.data(), ns) || upload(ctx, &l.slot2lex, s2l.data(), ns) ||
         upload(ctx, &l.lex2slot, l2s.data(), ng) || dalloc(ctx, &l.gval, ns) ||
         dalloc(ctx, &l.gtmp, std::max(ns, ng)) || upload(ctx, &l.dep_off, doff.data(), ns + 1) ||
-        upload(ctx, &l.dep, dep.data(), (int64_t)dep.size()) || dalloc(ctx, &l.gctr, ns + 1))
+        upload(ctx, &l.dep, dep.data(), (int64_t)dep.size()) || dalloc(ctx, &l.gctr, ns + 1) ||
+        upload(ctx, &l.vmask, vmask.data(), ns) || dalloc(ctx, &l.gpair, 2 * ns) ||
+        upload(ctx, &l.dbatch_off, l.batch_off.data(), maxb + 2))
       return -1;
     GMG_CHECK(ctx, cudaMemset(l.gval, 0, sizeof(double) * ns));
   } else {
@@ -825,6 +872,15 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     GMG_CHECK(ctx, cudaMallocHost(&l.x_h, sizeof(double) * (size_t)std::max<int64_t>(n, 1)));
   }
   l.ready = true;
+  // restriction masks need both levels of a pair
+  for (int cl = std::max(li, 1); cl <= std::min(li + 1, ctx->nlevels - 1); ++cl) {
+    DevLevel& fl = ctx->L[cl - 1];
+    DevLevel& clv = ctx->L[cl];
+    if (!fl.ready || !clv.ready) continue;
+    if (!clv.rmask && dalloc(ctx, &clv.rmask, clv.g.nodes)) return -1;
+    launch_restrict_mask(fl.g, fl.labels, clv.g, clv.labels, clv.rmask, ctx->stream);
+    GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  }
   return 0;
 }
 
@@ -1058,6 +1114,17 @@ int gmg_synchronize(gmg_ctx* ctx) {
 }
 
 int64_t gmg_launch_count(const gmg_ctx* ctx) { return ctx->launches; }
+
+int64_t gmg_debug_ghost_trace(gmg_ctx* ctx, int li, long long* host, int64_t cap) {
+  if (li < 0 || li >= ctx->nlevels) return fail(ctx, "bad level");
+  DevLevel& l = ctx->L[li];
+  if (!l.ghtrace) return 0;
+  const int64_t n = std::min<int64_t>(cap, 3 * l.nslots);
+  cudaSetDevice(ctx->device);
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  GMG_CHECK(ctx, cudaMemcpy(host, l.ghtrace, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+  return n;
+}
 
 int64_t gmg_debug_gs_trace(gmg_ctx* ctx, int li, long long* host, int64_t cap) {
   if (li < 0 || li >= ctx->nlevels) return fail(ctx, "bad level");

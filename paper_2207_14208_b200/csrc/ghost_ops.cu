@@ -42,68 +42,189 @@ __global__ void __launch_bounds__(256) ghost_batch_kernel(GhostArgs a, double* _
   u[node] = u[node] + a.dtau[s] * (a.gval[s] - dot);
 }
 
-__device__ __forceinline__ int ld_acquire_i(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+// (value, done tag) pairs: written with one 16-byte store, read with one
+// 16-byte load through L2 -- the value travels with its flag, so neither side
+// needs a memory barrier (gpu-scope release/acquire would drain the SM's
+// memory pipeline / flush its L1 on every ghost).
+__device__ __forceinline__ double2 ld_pair(const double* p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_i(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_pair(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v), "d"(1.0) : "memory");
+}
+__device__ __forceinline__ double wait_pair(const double* p, int backoff) {
+  double2 v = ld_pair(p);
+  while (v.y == 0.0) {
+    if (backoff) __nanosleep(backoff);
+    v = ld_pair(p);
+  }
+  return v.x;
 }
 
 // The whole ghost sweep in one launch, ordered by the sweep DAG instead of
-// batch barriers: warps claim 32-slot chunks in slot order (batch, lex); a
-// ghost waits (acquire) on the done flags of exactly the earlier ghosts it
-// reads or that read it, relaxes, stores, and releases its own flag.  Every
-// dependency lies in an earlier batch, hence an earlier chunk already held by
-// a running warp, so the sweep cannot deadlock, and each ghost sees the same
-// values as in the reference's lexicographic loop.  flags[nslots] is the
-// chunk cursor; all flags are zeroed before the launch.
+// batch barriers: warps claim 32-slot chunks in slot order (batch, lex).  A
+// ghost prefetches its weights and all 3^d stencil values, then takes the
+// new value of every earlier ghost it reads (vmask, in stencil order) from
+// that ghost's (value, tag) pair as soon as the tag is set, waits for the
+// earlier ghosts that read its own old value, relaxes, and publishes its new
+// value in u and in its pair.  Every dependency lies in an earlier batch,
+// hence an earlier chunk already held by a running warp, so the sweep cannot
+// deadlock, and each ghost sees the same values as in the reference's
+// lexicographic loop.  Pairs and the chunk cursor are zeroed before the launch.
 template <int D>
 __global__ void __launch_bounds__(256) ghost_persistent_kernel(GhostArgs a, double* __restrict__ u,
                                                                const int32_t* __restrict__ dep_off,
-                                                               const int32_t* __restrict__ dep, int* flags) {
+                                                               const int32_t* __restrict__ dep,
+                                                               const uint32_t* __restrict__ vmask,
+                                                               double* pair, int* cursor, int backoff,
+                                                               long long* gtrace) {
   constexpr int M = D == 3 ? 27 : 9;
   const int lane = threadIdx.x & 31;
   const int64_t nchunks = a.ng / 32;
   for (;;) {
     int chunk = 0;
-    if (lane == 0) chunk = atomicAdd(&flags[a.ng], 1);
+    if (lane == 0) chunk = atomicAdd(cursor, 1);
     chunk = __shfl_sync(0xffffffffu, chunk, 0);
     if (chunk >= nchunks) return;
     const int64_t s = (int64_t)chunk * 32 + lane;
     const int64_t node = a.node[s];
+    long long tg0 = 0, tg1 = 0;
+    if (gtrace) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tg0));
     if (node >= 0) {
       const int64_t base = a.base[s];
       double x[M], y[M];
 #pragma unroll
-      for (int j = 0; j < M; ++j) x[j] = __ldg(a.w + (int64_t)j * a.ng + s);
-      const double gv = a.gval[s], dt = a.dtau[s];
-      const int d1 = dep_off[s + 1];
-      for (int k = dep_off[s]; k < d1; ++k) {
-        const int* f = flags + dep[k];
-        while (ld_acquire_i(f) == 0) {
-        }
+      for (int j = 0; j < M; ++j) {
+        x[j] = __ldg(a.w + (int64_t)j * a.ng + s);
+        y[j] = __ldcg(u + base + block_offset<D>(a.g, j));
       }
+      const double gv = a.gval[s], dt = a.dtau[s], uo = __ldcg(u + node);
+      const uint32_t vm = vmask[s];
+      const int k0 = dep_off[s];
+      const int d1 = dep_off[s + 1];
+      // all dependency pairs are (re)loaded together each round -- one L2
+      // round trip per round -- until every tag is set
+      {
+        constexpr int WMAX = 8;  // wait-only dependencies polled together
+        const int nv = __popc(vm);
+        const int kw = k0 + nv, nw = min(d1 - kw, WMAX);
+        for (;;) {
+          double tg[M], wt[WMAX];
+          int k = k0;
 #pragma unroll
-      for (int j = 0; j < M; ++j) y[j] = __ldcg(u + base + block_offset<D>(a.g, j));
+          for (int j = 0; j < M; ++j) {
+            tg[j] = 1.0;
+            if ((vm >> j) & 1u) {
+              const double2 pv = ld_pair(pair + 2 * (int64_t)dep[k++]);
+              y[j] = pv.x;
+              tg[j] = pv.y;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < WMAX; ++q) wt[q] = q < nw ? ld_pair(pair + 2 * (int64_t)dep[kw + q]).y : 1.0;
+          bool all = true;
+#pragma unroll
+          for (int j = 0; j < M; ++j) all = all && tg[j] != 0.0;
+#pragma unroll
+          for (int q = 0; q < WMAX; ++q) all = all && wt[q] != 0.0;
+          if (all) break;
+          if (backoff) __nanosleep(backoff);
+        }
+        for (int k = kw + WMAX; k < d1; ++k) wait_pair(pair + 2 * (int64_t)dep[k], backoff);
+      }
+      if (gtrace) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tg1));
       const double dot = blas_ddot<M>(x, y);
-      __stcg(u + node, __ldcg(u + node) + dt * (gv - dot));
-      st_release_i(flags + s, 1);
+      const double nv = uo + dt * (gv - dot);
+      __stcg(u + node, nv);
+      st_pair(pair + 2 * s, nv);
+    }
+    if (gtrace) {
+      long long tg2;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tg2));
+      gtrace[3 * s] = tg0;
+      gtrace[3 * s + 1] = tg1;
+      gtrace[3 * s + 2] = tg2;
     }
   }
 }
 
-void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_off, const int32_t* dep, int* flags,
-                             int sms, cudaStream_t st) {
+// Level-synchronous variant: one CTA per SM walks the sweep batches (DAG
+// levels) in order; the CTAs split each batch's slots, then meet at a
+// grid-wide counter (one polling thread per CTA, with back-off) before the
+// next batch.  Values of earlier ghosts still come from their (value, tag)
+// pairs -- the counter only throttles polling (its increments need no fence:
+// a pair that is not visible yet is simply waited for).
+template <int D>
+__global__ void __launch_bounds__(1024) ghost_levels_kernel(GhostArgs a, double* __restrict__ u,
+                                                            const int64_t* __restrict__ boff, int nbatch,
+                                                            const int32_t* __restrict__ dep_off,
+                                                            const int32_t* __restrict__ dep,
+                                                            const uint32_t* __restrict__ vmask, double* pair,
+                                                            int* counter) {
+  constexpr int M = D == 3 ? 27 : 9;
+  for (int b = 0; b < nbatch; ++b) {
+    const int64_t lo = boff[b], hi = boff[b + 1];
+    for (int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < hi;
+         s += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t node = a.node[s];
+      if (node < 0) continue;
+      const int64_t base = a.base[s];
+      double x[M], y[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        x[j] = __ldg(a.w + (int64_t)j * a.ng + s);
+        y[j] = __ldcg(u + base + block_offset<D>(a.g, j));
+      }
+      const double gv = a.gval[s], dt = a.dtau[s], uo = __ldcg(u + node);
+      const uint32_t vm = vmask[s];
+      int k = dep_off[s];
+#pragma unroll
+      for (int j = 0; j < M; ++j)
+        if ((vm >> j) & 1u) y[j] = wait_pair(pair + 2 * (int64_t)dep[k++], 0);
+      const double dot = blas_ddot<M>(x, y);
+      const double nv = uo + dt * (gv - dot);
+      __stcg(u + node, nv);
+      st_pair(pair + 2 * s, nv);
+    }
+    if (b + 1 == nbatch) break;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicAdd(counter, 1);
+      const int target = (b + 1) * (int)gridDim.x;
+      int v;
+      for (;;) {
+        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+        if (v >= target) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+void launch_ghost_levels(const GhostArgs& a, double* u, const int64_t* boff, int nbatch, const int32_t* dep_off,
+                         const int32_t* dep, const uint32_t* vmask, double* pair, int* counter, int sms,
+                         cudaStream_t st) {
+  if (a.g.d == 3)
+    ghost_levels_kernel<3><<<sms, 1024, 0, st>>>(a, u, boff, nbatch, dep_off, dep, vmask, pair, counter);
+  else
+    ghost_levels_kernel<2><<<sms, 1024, 0, st>>>(a, u, boff, nbatch, dep_off, dep, vmask, pair, counter);
+}
+
+void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_off, const int32_t* dep,
+                             const uint32_t* vmask, double* pair, int* cursor, int sms, int blocks_per_sm,
+                             int backoff, long long* gtrace, cudaStream_t st) {
   const int64_t warps = a.ng / 32;
-  int blocks = (int)std::min<int64_t>((warps + 7) / 8, (int64_t)sms * 8);
+  int blocks = (int)std::min<int64_t>((warps + 7) / 8, (int64_t)sms * blocks_per_sm);
   if (blocks < 1) blocks = 1;
   if (a.g.d == 3)
-    ghost_persistent_kernel<3><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, flags);
+    ghost_persistent_kernel<3><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace);
   else
-    ghost_persistent_kernel<2><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, flags);
+    ghost_persistent_kernel<2><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace);
 }
+
 
 
 void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st) {

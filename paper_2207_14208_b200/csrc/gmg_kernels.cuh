@@ -62,8 +62,12 @@ size_t gs_diag_smem();
 void configure_gs_kernels();  // set max dynamic shared memory of the GS / GEMV kernels
 
 void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st);
-void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_off, const int32_t* dep, int* flags,
-                             int sms, cudaStream_t st);
+void launch_ghost_levels(const GhostArgs& a, double* u, const int64_t* boff, int nbatch, const int32_t* dep_off,
+                         const int32_t* dep, const uint32_t* vmask, double* pair, int* counter, int sms,
+                         cudaStream_t st);
+void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_off, const int32_t* dep,
+                             const uint32_t* vmask, double* pair, int* cursor, int sms, int blocks_per_sm,
+                             int backoff, long long* gtrace, cudaStream_t st);
 void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,
                            unsigned long long* maxbits, cudaStream_t st);
 void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,
@@ -71,9 +75,10 @@ void launch_residual_interior(const Geom& g, const uint8_t* labels, const double
                               cudaStream_t st);
 void launch_band_bfs(const BandArgs& a, double* x, int64_t lo, int64_t hi, cudaStream_t st);
 void launch_band_transport(const BandArgs& a, double* x, cudaStream_t st);
-void launch_restrict_interior(const Geom& gf, const uint8_t* lab_f, const double* r_f,
-                              const Geom& gc, const uint8_t* lab_c, double* f_c,
-                              cudaStream_t st);
+void launch_restrict_interior(const Geom& gf, const double* r_f, const Geom& gc, const uint32_t* rmask,
+                              double* f_c, cudaStream_t st);
+void launch_restrict_mask(const Geom& gf, const uint8_t* lab_f, const Geom& gc, const uint8_t* lab_c,
+                          uint32_t* rmask, cudaStream_t st);
 void launch_restrict_ghost(const Geom& gf, const uint8_t* lab_f, const double* r_ext,
                            const GhostArgs& coarse, double* gval_c, cudaStream_t st);
 void launch_interp_add(const Geom& gf, const uint8_t* lab_f, double* u_f, const Geom& gc,

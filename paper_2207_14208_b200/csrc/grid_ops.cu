@@ -5,6 +5,9 @@
 // All are HBM-streaming fp64 kernels (no tensor-core work on this path);
 // the arithmetic order restates the reference op by op (file:line at each
 // kernel).
+#include <algorithm>
+#include <cstdlib>
+
 #include "gmg_kernels.cuh"
 
 namespace gmg {
@@ -33,6 +36,8 @@ unsigned grid_for(int64_t n, int threads, int64_t cap = 148 * 16) {
   return (unsigned)b;
 }
 
+constexpr int IC = 2;  // columns per thread of the row kernels
+
 }  // namespace
 
 // residual_internal (smoothing.py:111-118) into a full array:
@@ -60,14 +65,122 @@ __global__ void __launch_bounds__(256) residual_interior_kernel(Geom g, const ui
   block_max_commit(am, maxbits);
 }
 
+// 3-D version streaming along planes: a CTA owns a 32-column x 8-row tile
+// and marches over the planes, holding the planes below/above its own nodes
+// in registers and the current plane's tile (+1 halo) in shared memory, so u
+// is read from HBM about once.  Same arithmetic order as above.  With
+// r == nullptr only the maximum is produced (the residual-norm pass).
+constexpr int RT_J = 8, RT_K = 32;
+__global__ void __launch_bounds__(256) residual_stream3_kernel(Geom g, const uint8_t* __restrict__ lab,
+                                                               const double* __restrict__ u,
+                                                               const double* __restrict__ f,
+                                                               double* __restrict__ r,
+                                                               unsigned long long* maxbits) {
+  __shared__ double tile[RT_J + 2][RT_K + 2];
+  const int N = (int)g.N;
+  const int tk = threadIdx.x & 31, tj = threadIdx.x >> 5;
+  const int k = 1 + (int)blockIdx.x * RT_K + tk;   // column
+  const int j = 1 + (int)blockIdx.y * RT_J + tj;   // row
+  const bool mine = k <= N - 1 && j <= N - 1;
+  const int kc = min(k, N), jc = min(j, N);        // clamped (in-grid) position
+  const int64_t col = (int64_t)kc + OFF;
+  auto at = [&](int i, int jj) -> int64_t { return ((int64_t)i * g.n + jj) * g.P; };
+  // halo cells of the tile: 2 x RT_K row cells + 2 x (RT_J + 2) column cells
+  auto load_tile = [&](int i) {
+    tile[tj + 1][tk + 1] = u[at(i, jc) + col];
+    const int t = threadIdx.x;
+    if (t < 2 * RT_K) {  // rows j0-1 and j0+RT_J
+      const int hj = t < RT_K ? (int)blockIdx.y * RT_J : min((int)blockIdx.y * RT_J + RT_J + 1, N);
+      const int hk = min(1 + (int)blockIdx.x * RT_K + (t & (RT_K - 1)), N);
+      tile[t < RT_K ? 0 : RT_J + 1][(t & (RT_K - 1)) + 1] = u[at(i, hj) + hk + OFF];
+    } else if (t < 2 * RT_K + 2 * (RT_J + 2)) {  // columns k0-1 and k0+RT_K
+      const int q = t - 2 * RT_K, side = q / (RT_J + 2), rr = q % (RT_J + 2);
+      const int hj = min((int)blockIdx.y * RT_J + rr, N);
+      const int hk = side == 0 ? (int)blockIdx.x * RT_K : min((int)blockIdx.x * RT_K + RT_K + 1, N);
+      tile[rr][side == 0 ? 0 : RT_K + 1] = u[at(i, hj) + hk + OFF];
+    }
+  };
+  double um = u[at(0, jc) + col];
+  load_tile(1);
+  __syncthreads();
+  double uc = tile[tj + 1][tk + 1];
+  double am = 0.0;
+  for (int i = 1; i <= N - 1; ++i) {
+    const double up = u[at(i + 1, jc) + col];
+    const int64_t pos = at(i, jc) + col;
+    if (mine && lab[pos] == INTERNAL) {
+      double s = ((((um + up) + tile[tj][tk + 1]) + tile[tj + 2][tk + 1]) + tile[tj + 1][tk]) + tile[tj + 1][tk + 2];
+      s = s + 0.0;
+      const double v = (f[pos] - g.c * uc) + s / g.h2;
+      if (r) r[pos] = v;
+      am = (__double_as_longlong(fabs(v)) > __double_as_longlong(am)) ? fabs(v) : am;
+    }
+    __syncthreads();
+    if (i < N - 1) load_tile(i + 1);
+    __syncthreads();
+    um = uc;
+    uc = up;
+  }
+  block_max_commit(am, maxbits);
+}
+
+// 3-D row version: interior rows only (every stencil access in bounds), IC
+// columns per thread with all loads issued first.
+template <bool WRITE>
+__global__ void __launch_bounds__(128) residual_rows3_kernel(Geom g, const uint8_t* __restrict__ lab,
+                                                             const double* __restrict__ u,
+                                                             const double* __restrict__ f,
+                                                             double* __restrict__ r,
+                                                             unsigned long long* maxbits) {
+  const int N = (int)g.N;
+  const int inner = N - 1;
+  const int64_t nrows = (int64_t)inner * inner;
+  double am = 0.0;
+  for (int64_t rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
+    const int64_t i = rr / inner + 1, j = rr % inner + 1;
+    const int64_t base = (i * g.n + j) * g.P + OFF;
+    for (int k0 = 1 + threadIdx.x; k0 <= N - 1; k0 += IC * blockDim.x) {
+      double s[IC], uc[IC], fv[IC];
+      uint8_t L[IC];
+#pragma unroll
+      for (int q = 0; q < IC; ++q) {
+        const int kk = k0 + q * (int)blockDim.x;
+        const int kc = kk <= N - 1 ? kk : N - 1;
+        const int64_t p = base + kc;
+        L[q] = kk <= N - 1 ? lab[p] : (uint8_t)PAD;  // out of the row: never written
+        uc[q] = u[p];
+        fv[q] = f[p];
+        s[q] = ((((u[p - g.s0] + u[p + g.s0]) + u[p - g.s1]) + u[p + g.s1]) + u[p - 1]) + u[p + 1];
+      }
+#pragma unroll
+      for (int q = 0; q < IC; ++q) {
+        if (L[q] != INTERNAL) continue;
+        const double sv = s[q] + 0.0;
+        const double v = (fv[q] - g.c * uc[q]) + sv / g.h2;
+        if (WRITE) r[base + k0 + q * (int)blockDim.x] = v;
+        am = (__double_as_longlong(fabs(v)) > __double_as_longlong(am)) ? fabs(v) : am;
+      }
+    }
+  }
+  block_max_commit(am, maxbits);
+}
+
 void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,
                               const double* f, double* r, unsigned long long* maxbits,
                               cudaStream_t st) {
-  const unsigned blocks = grid_for(g.nodes, 256);
-  if (g.d == 3)
-    residual_interior_kernel<3><<<blocks, 256, 0, st>>>(g, labels, u, f, r, maxbits);
-  else
-    residual_interior_kernel<2><<<blocks, 256, 0, st>>>(g, labels, u, f, r, maxbits);
+  if (g.d == 3 && getenv("GMG_RES_STREAM")) {
+    dim3 grid((unsigned)((g.N - 1 + RT_K - 1) / RT_K), (unsigned)((g.N - 1 + RT_J - 1) / RT_J));
+    residual_stream3_kernel<<<grid, 256, 0, st>>>(g, labels, u, f, r, maxbits);
+  } else if (g.d == 3) {
+    const int64_t nrows = (g.N - 1) * (g.N - 1);
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 16));
+    if (r)
+      residual_rows3_kernel<true><<<blocks, 128, 0, st>>>(g, labels, u, f, r, maxbits);
+    else
+      residual_rows3_kernel<false><<<blocks, 128, 0, st>>>(g, labels, u, f, r, maxbits);
+  } else {
+    residual_interior_kernel<2><<<grid_for(g.nodes, 256), 256, 0, st>>>(g, labels, u, f, r, maxbits);
+  }
 }
 
 template <int D>
@@ -88,105 +201,183 @@ __device__ __forceinline__ double fw_w(int e) {
 // InteriorRestriction.apply (transfer.py:64-93): coarse internal node at m
 // takes pairwise(w * r[3^D fine block around 2m]); w = full weighting unless
 // the block holds a ghost/inactive node, then 1/count on its internal nodes.
+// Row loop: a CTA takes coarse rows (grid-stride), its threads the columns
+// of the row.  The fine-label pattern of every coarse node's 3^D block is
+// precomputed once per hierarchy (restrict_mask_kernel): bit e = fine node e
+// of the block is internal, bit 30 = the coarse node is internal, bit 31 =
+// the block holds a ghost / inactive node ("mixed").  The 3^D residual
+// loads do not depend on it, so they are all in flight together.
+constexpr uint32_t RM_COARSE = 1u << 30, RM_MIXED = 1u << 31;
+
 template <int D>
-__global__ void __launch_bounds__(256) restrict_interior_kernel(Geom gf, const uint8_t* __restrict__ lab_f,
-                                                                const double* __restrict__ r_f, Geom gc,
-                                                                const uint8_t* __restrict__ lab_c,
-                                                                double* __restrict__ f_c) {
+__device__ __forceinline__ int64_t block_off(const Geom& gf, int e) {
+  if (D == 3) return (int64_t)(e / 9 - 1) * gf.s0 + (int64_t)((e / 3) % 3 - 1) * gf.s1 + (e % 3 - 1);
+  return (int64_t)(e / 3 - 1) * gf.s0 + (e % 3 - 1);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) restrict_mask_kernel(Geom gf, const uint8_t* __restrict__ lab_f, Geom gc,
+                                                            const uint8_t* __restrict__ lab_c,
+                                                            uint32_t* __restrict__ rmask) {
   constexpr int M = D == 3 ? 27 : 9;
-  for (int64_t ic = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ic < gc.nodes;
-       ic += (int64_t)gridDim.x * blockDim.x) {
-    if (lab_c[ic] != INTERNAL) continue;
-    int64_t mc[3];
-    pos_multi(gc, ic, mc);
-#pragma unroll
-    for (int k = 0; k < D; ++k) mc[k] *= 2;
-    const int64_t center = multi_pos(gf, mc);
-    int64_t blk[M];
-    bool mixed = false;
-    int cnt = 0;
-    uint32_t internal_bits = 0;
-#pragma unroll
-    for (int e = 0; e < M; ++e) {
-      int64_t off;
-      if (D == 3)
-        off = (int64_t)(e / 9 - 1) * gf.s0 + (int64_t)((e / 3) % 3 - 1) * gf.s1 + (e % 3 - 1);
-      else
-        off = (int64_t)(e / 3 - 1) * gf.s0 + (e % 3 - 1);
-      blk[e] = center + off;
-      const uint8_t L = lab_f[blk[e]];
-      mixed |= (L == GHOST || L == INACTIVE);
-      if (L == INTERNAL) {
-        ++cnt;
-        internal_bits |= 1u << e;
+  const int nc = (int)gc.n;
+  const int64_t nrows = D == 3 ? (int64_t)nc * nc : nc;
+  for (int64_t rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
+    const int I = D == 3 ? (int)(rr / nc) : 0;
+    const int J = D == 3 ? (int)(rr % nc) : (int)rr;
+    for (int K = threadIdx.x; K < nc; K += blockDim.x) {
+      const int64_t ic = rr * gc.P + K + OFF;
+      uint32_t m = 0;
+      if (lab_c[ic] == INTERNAL) {
+        const int64_t frow = D == 3 ? (int64_t)(2 * I) * gf.n + 2 * J : 2 * J;
+        const int64_t center = frow * gf.P + 2 * K + OFF;
+        m = RM_COARSE;
+        for (int e = 0; e < M; ++e) {
+          const uint8_t L = lab_f[center + block_off<D>(gf, e)];
+          if (L == GHOST || L == INACTIVE) m |= RM_MIXED;
+          if (L == INTERNAL) m |= 1u << e;
+        }
       }
+      rmask[ic] = m;
     }
-    double p[M];
-    if (mixed) {
-      const double dc = (double)cnt;
-#pragma unroll
-      for (int e = 0; e < M; ++e) p[e] = (((internal_bits >> e) & 1u) ? 1.0 : 0.0) / dc * r_f[blk[e]];
-    } else {
-#pragma unroll
-      for (int e = 0; e < M; ++e) p[e] = fw_w<D>(e) * r_f[blk[e]];
-    }
-    f_c[ic] = np_sum<M>(p);
   }
 }
 
-void launch_restrict_interior(const Geom& gf, const uint8_t* lab_f, const double* r_f,
-                              const Geom& gc, const uint8_t* lab_c, double* f_c,
-                              cudaStream_t st) {
-  const unsigned blocks = grid_for(gc.nodes, 256);
-  if (gf.d == 3)
-    restrict_interior_kernel<3><<<blocks, 256, 0, st>>>(gf, lab_f, r_f, gc, lab_c, f_c);
+void launch_restrict_mask(const Geom& gf, const uint8_t* lab_f, const Geom& gc, const uint8_t* lab_c,
+                          uint32_t* rmask, cudaStream_t st) {
+  const int64_t nrows = gc.d == 3 ? gc.n * gc.n : gc.n;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 8));
+  if (gc.d == 3)
+    restrict_mask_kernel<3><<<blocks, 256, 0, st>>>(gf, lab_f, gc, lab_c, rmask);
   else
-    restrict_interior_kernel<2><<<blocks, 256, 0, st>>>(gf, lab_f, r_f, gc, lab_c, f_c);
+    restrict_mask_kernel<2><<<blocks, 256, 0, st>>>(gf, lab_f, gc, lab_c, rmask);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 3) restrict_interior_kernel(Geom gf, const double* __restrict__ r_f, Geom gc,
+                                                                const uint32_t* __restrict__ rmask,
+                                                                double* __restrict__ f_c) {
+  constexpr int M = D == 3 ? 27 : 9;
+  const int nc = (int)gc.n;
+  const int inner = nc - 2;  // rows/columns 1 .. N_c - 1 can hold internal nodes
+  const int64_t nrows = D == 3 ? (int64_t)inner * inner : inner;
+  for (int64_t rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
+    const int I = D == 3 ? (int)(rr / inner) + 1 : 0;
+    const int J = D == 3 ? (int)(rr % inner) + 1 : (int)rr + 1;
+    const int64_t crow = D == 3 ? (int64_t)I * nc + J : J;
+    const int64_t frow = D == 3 ? (int64_t)(2 * I) * gf.n + 2 * J : 2 * J;
+    for (int K = 1 + threadIdx.x; K <= nc - 2; K += blockDim.x) {
+      const int64_t ic = crow * gc.P + K + OFF;
+      const uint32_t m = rmask[ic];
+      if (!(m & RM_COARSE)) continue;
+      const double* rc = r_f + frow * gf.P + 2 * K + OFF;
+      double p[M];
+#pragma unroll
+      for (int e = 0; e < M; ++e) p[e] = rc[block_off<D>(gf, e)];
+      if (m & RM_MIXED) {
+        const double dc = (double)__popc(m & ((1u << M) - 1u));
+#pragma unroll
+        for (int e = 0; e < M; ++e) p[e] = (((m >> e) & 1u) ? 1.0 : 0.0) / dc * p[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < M; ++e) p[e] = fw_w<D>(e) * p[e];
+      }
+      f_c[ic] = np_sum<M>(p);
+    }
+  }
+}
+
+void launch_restrict_interior(const Geom& gf, const double* r_f, const Geom& gc, const uint32_t* rmask,
+                              double* f_c, cudaStream_t st) {
+  const int64_t inner = gc.n - 2;
+  const int64_t nrows = gf.d == 3 ? inner * inner : inner;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 8));
+  if (gf.d == 3)
+    restrict_interior_kernel<3><<<blocks, 256, 0, st>>>(gf, r_f, gc, rmask, f_c);
+  else
+    restrict_interior_kernel<2><<<blocks, 256, 0, st>>>(gf, r_f, gc, rmask, f_c);
 }
 
 // ErrorInterpolation + correction (transfer.py:124-151, solver.py:198):
 // u += sum_c w_c e[src_c] on internal and ghost fine nodes; corner c of
 // {0,1}^D in C order, w_c = prod_k (odd_k ? 1/2 : [c_k == 0]).
+// Row loop over fine rows (grid-stride); each thread takes IC columns of the
+// row (stride blockDim) and issues all of their loads before any arithmetic,
+// so enough bytes are in flight to cover HBM latency.  The coarse rows and
+// the plane/row weights of the 2^D corners are per-row constants; only the
+// column parity varies along the row.
 template <int D>
-__global__ void __launch_bounds__(256) interp_add_kernel(Geom gf, const uint8_t* __restrict__ lab_f,
+__global__ void __launch_bounds__(128) interp_add_kernel(Geom gf, const uint8_t* __restrict__ lab_f,
                                                          double* __restrict__ u, Geom gc,
                                                          const double* __restrict__ e) {
   constexpr int NC = 1 << D;
-  const int64_t sc[3] = {gc.s0, gc.s1, gc.s2};
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < gf.nodes;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint8_t L = lab_f[i];
-    if (L != INTERNAL && L != GHOST) continue;
-    int64_t m[3], half[3];
-    pos_multi(gf, i, m);
+  const int nf = (int)gf.n;
+  const int64_t nrows = D == 3 ? (int64_t)nf * nf : nf;
+  for (int64_t rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
+    const int ii = D == 3 ? (int)(rr / nf) : 0;
+    const int jj = D == 3 ? (int)(rr % nf) : (int)rr;
+    // corner rows (c0, c1) and their weights; 2-D uses c0 = 0 only
+    const double* erow[2][2];
+    double wrow[2][2];
+    {
+      const int oi = ii & 1, oj = jj & 1;
+      const int64_t hi = ii >> 1, hj = jj >> 1;
 #pragma unroll
-    for (int k = 0; k < D; ++k) half[k] = m[k] / 2;
-    const int64_t cbase = multi_pos(gc, half);
-    double p[NC];
+      for (int c0 = 0; c0 < 2; ++c0)
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      double w = 1.0;
-      int64_t src = cbase;
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        const int off = (c >> (D - 1 - k)) & 1;
-        const int odd = (int)(m[k] & 1);
-        w = w * (odd ? 0.5 : (off == 0 ? 1.0 : 0.0));
-        src += (odd ? off : 0) * sc[k];
-      }
-      p[c] = w * e[src];
+        for (int c1 = 0; c1 < 2; ++c1) {
+          const int64_t ri = hi + (oi ? c0 : 0), rj = hj + (oj ? c1 : 0);
+          erow[c0][c1] = e + (D == 3 ? (ri * gc.n + rj) * gc.P : rj * gc.P) + OFF;
+          const double wi = oi ? 0.5 : (c0 == 0 ? 1.0 : 0.0);
+          const double wj = oj ? 0.5 : (c1 == 0 ? 1.0 : 0.0);
+          wrow[c0][c1] = D == 3 ? (1.0 * wi) * wj : 1.0 * wj;
+        }
     }
-    u[i] = u[i] + np_sum<NC>(p);
+    double* urow = u + rr * gf.P + OFF;
+    const uint8_t* lrow = lab_f + rr * gf.P + OFF;
+    for (int k0 = threadIdx.x; k0 < nf; k0 += IC * blockDim.x) {
+      double uv[IC], p[IC][NC];
+      uint8_t L[IC];
+#pragma unroll
+      for (int q = 0; q < IC; ++q) {
+        const int kk = k0 + q * (int)blockDim.x;
+        const bool in = kk < nf;
+        const int kc = in ? kk : 0;
+        L[q] = in ? lrow[kc] : (uint8_t)PAD;  // out of the row: never written
+        uv[q] = urow[kc];
+        const int ok = kc & 1, hk = kc >> 1, col1 = hk + ok;
+        const double wk0 = ok ? 0.5 : 1.0, wk1 = ok ? 0.5 : 0.0;
+        if (D == 3) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int c0 = c >> 2, c1 = (c >> 1) & 1, c2 = c & 1;
+            p[q][c] = (wrow[c0][c1] * (c2 ? wk1 : wk0)) * erow[c0][c1][c2 ? col1 : hk];
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int c1 = c >> 1, c2 = c & 1;
+            p[q][c] = (wrow[0][c1] * (c2 ? wk1 : wk0)) * erow[0][c1][c2 ? col1 : hk];
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < IC; ++q) {
+        if (L[q] != INTERNAL && L[q] != GHOST) continue;
+        urow[k0 + q * (int)blockDim.x] = uv[q] + np_sum<NC>(p[q]);
+      }
+    }
   }
 }
 
 void launch_interp_add(const Geom& gf, const uint8_t* lab_f, double* u_f, const Geom& gc,
                        const double* e_c, cudaStream_t st) {
-  const unsigned blocks = grid_for(gf.nodes, 256);
+  const int64_t nrows = gf.d == 3 ? gf.n * gf.n : gf.n;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 16));
   if (gf.d == 3)
-    interp_add_kernel<3><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
+    interp_add_kernel<3><<<blocks, 128, 0, st>>>(gf, lab_f, u_f, gc, e_c);
   else
-    interp_add_kernel<2><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
+    interp_add_kernel<2><<<blocks, 128, 0, st>>>(gf, lab_f, u_f, gc, e_c);
 }
 
 // Band BFS group (transfer.py:245-246): x_i = (sum_k x[nbr_k] * mask_k) /
