@@ -21,3 +21,5 @@ for l, p in enumerate(plans):
     cnt = np.bincount(b)
     print(f"L{l} N={p.N}: ghosts {p.n_ghosts}, batches {len(cnt)}, per-batch max {cnt.max()} "
           f"median {int(np.median(cnt))}, first 8 {cnt[:8].tolist()}, last 8 {cnt[-8:].tolist()}")
+for l, p in enumerate(plans):
+    print(f"L{l} N={p.N}: band nodes {len(p.band_idx)}, bfs groups {list(np.asarray(p.bfs_len))}")
