@@ -204,7 +204,7 @@ class Context:
 
     def gs_trace(self, level, ntasks):
         """GS task timeline of the last sweep on `level` (GMG_GS_TRACE=1)."""
-        out = np.zeros((ntasks, 16), dtype=np.int64)
+        out = np.zeros((ntasks, 24), dtype=np.int64)
         n = self.lib.gmg_debug_gs_trace(self.ctx, level, out.ctypes.data, out.size)
         return out if n else None
 

@@ -391,8 +391,8 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
   a.variant = ctx->gs_variant;
   for (int i = 0; i < 4; ++i) a.sleep_ns[i] = ctx->gs_sleep[i];
   if (ctx->gs_trace && (l.ws_gs || l.diag_gs)) {
-    if (!l.trace && dalloc(ctx, &l.trace, (int64_t)l.ntasks * 16)) return -1;
-    GMG_CHECK(ctx, cudaMemsetAsync(l.trace, 0, sizeof(long long) * (size_t)l.ntasks * 16, ctx->stream));
+    if (!l.trace && dalloc(ctx, &l.trace, (int64_t)l.ntasks * 24)) return -1;
+    GMG_CHECK(ctx, cudaMemsetAsync(l.trace, 0, sizeof(long long) * (size_t)l.ntasks * 24, ctx->stream));
     a.trace = l.trace;
   }
   if (ctx->gs_max_tasks > 0) a.ntasks = std::min(a.ntasks, ctx->gs_max_tasks);  // timing experiments only
@@ -1130,7 +1130,7 @@ int64_t gmg_debug_gs_trace(gmg_ctx* ctx, int li, long long* host, int64_t cap) {
   if (li < 0 || li >= ctx->nlevels) return fail(ctx, "bad level");
   DevLevel& l = ctx->L[li];
   if (!l.trace) return 0;
-  const int64_t n = std::min<int64_t>(cap, (int64_t)l.ntasks * 16);
+  const int64_t n = std::min<int64_t>(cap, (int64_t)l.ntasks * 24);
   cudaSetDevice(ctx->device);
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   GMG_CHECK(ctx, cudaMemcpy(host, l.trace, sizeof(long long) * n, cudaMemcpyDeviceToHost));

@@ -52,7 +52,7 @@ constexpr int RFL = 80;  // f / mask ring lines (+ 8 mirrored rows)
 constexpr int NUB = 16, NFB = 16;  // mbarrier rings
 constexpr int HDEPTH = 8;                  // halo batches in flight
 #ifndef GS_PFD
-#define GS_PFD 16
+#define GS_PFD 4
 #endif
 constexpr int PFD = GS_PFD;                // L2 prefetch distance (batches)
 
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
     // read is as the plane below of line L + PL by lane 31 (3-D), or as the left
     // neighbour of lane 31 (2-D)
     constexpr int DEADLAG = D == 3 ? PL + 31 : 32;
-    long long* const tr = a.trace ? a.trace + (int64_t)tid * 16 : nullptr;
+    long long* const tr = a.trace ? a.trace + (int64_t)tid * 24 : nullptr;
 
     if (warp == 0) {
       // ============================ compute ==============================
@@ -452,6 +452,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         f0 = f8;
         __syncwarp();
         if (lane == 0) st_flag(&S.cons, 8 * k + 7);
+        if (tr && lane == 0 && k == 68) tr[17] = gtimer();  // compute: line 519 finished by lane 31
         if (tr && lane == 0 && (k == 64 || k == 512)) tr[k == 64 ? 5 : 7] = gtimer();
       }
       if (tr && lane == 0) {
@@ -669,11 +670,23 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
           issue(hs, hvA, uwA);
           ++hi;
         }
-        if (hi == hs + 1 && hi < NHq && ready(hi, true)) {
+        // the progress poll for batch hs+1 is in flight while batch hs is stored
+        // (its result is consumed afterwards; the shared-memory flags carry no
+        // fence, so nothing waits for the outstanding load)
+        const bool want = hi == hs + 1 && hi < NHq;
+        int pL = seenL, pU = seenU;
+        if (want) {
+          if (lprog && seenL < min(8 * hi + 8, nLines)) pL = ld_relaxed(lprog);
+          const int Lu = up_line(hi);
+          if (uprog && Lu >= 0 && seenU < Lu + PL) pU = ld_relaxed(uprog);
+        }
+        store(hs, hvA, uwA);
+        seenL = max(seenL, pL);
+        seenU = max(seenU, pU);
+        if (want && ready(hi, false)) {
           issue(hi, hvB, uwB);
           ++hi;
         }
-        store(hs, hvA, uwA);
         ++hs;
         hvA = hvB;
         uwA = uwB;
@@ -692,6 +705,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         const int cs = ld_flag(&S.cons);
         bool did = false;
         if (w < NWq && cs >= 8 * w + 7 + 31) {
+          if (tr && lane == 0 && w == 64) tr[16] = gtimer();  // writer: batch 64 ready
           if (lane == 0) bulk_wait_read<0>();  // staging free
           __syncwarp();
 #pragma unroll

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(64, 1) gs_ws_kernel(GsArgs a, const __grid_con
       return L + 1;
     };
     const int last = nLines + 30;  // last consumer step
-    long long* const tr = a.trace ? a.trace + (int64_t)tid * 16 : nullptr;
+    long long* const tr = a.trace ? a.trace + (int64_t)tid * 24 : nullptr;
 
     if (warp == 1) {
       // =============================== producer ===========================

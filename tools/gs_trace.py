@@ -118,6 +118,10 @@ if d == 3 and nt == len(tasks):
           f"  store-begin {med([(stb[k] - pub[(k[0]-1, k[1])]) / 1e3 for k in ks]):.2f}"
           f"  stored {med([(hst[k] - pub[(k[0]-1, k[1])]) / 1e3 for k in ks]):.2f}"
           f"  compute sees {med([(cav[k] - pub[(k[0]-1, k[1])]) / 1e3 for k in ks]):.2f}")
+    c68 = {k: tr[i, 17] for k, i in idx.items()}
+    wr = {k: tr[i, 16] for k, i in idx.items()}
+    print(f"writer (us, median): line 519 done -> writer starts batch 64 {med([(wr[k] - c68[k]) / 1e3 for k in idx]):.2f}; "
+          f"-> flag issued {med([(pub[k] - wr[k]) / 1e3 for k in idx]):.2f}")
     print(f"writer wait for store completion: {tr[:, 13].mean() / (lines / 8):.0f} cycles/batch")
     rate = (t512[(0, 0)] - t64[(0, 0)]) / (448 * 8)
     print(f"task (0,0) step time between batches 64 and 512: {rate * 1e3:.1f} ns")
