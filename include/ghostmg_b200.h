@@ -137,6 +137,9 @@ int64_t gmg_debug_gs_trace(gmg_ctx *ctx, int level, long long *host, int64_t cap
 /* Diagnostics: ghost-sweep timeline (GMG_GS_TRACE=1), 3 int64 per sweep slot
  * (claimed, dependencies met, stored; globaltimer ns) of the last sweep. */
 int64_t gmg_debug_ghost_trace(gmg_ctx *ctx, int level, long long *host, int64_t cap);
+/* Diagnostics: GS loader / writer back-off (4 values, ns; NULL keeps them)
+ * and implementation variant (< 0 keeps it) for the following sweeps. */
+int gmg_debug_gs_knobs(gmg_ctx *ctx, const int *sleep_ns, int variant);
 /* Device bytes held by the context. */
 int64_t gmg_device_bytes(const gmg_ctx *ctx);
 

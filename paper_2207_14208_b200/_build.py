@@ -31,16 +31,19 @@ def needs_build():
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(verbose=False, force=False):
-    if not force and not needs_build():
+def build(verbose=False, force=False, csrc=CSRC, lib=LIB):
+    """Compile `csrc` into `lib` (an alternate source tree / output path is
+    for A/B experiments with tools/build_alt.sh)."""
+    if not force and lib == LIB and not needs_build():
         return LIB
     objs = []
-    build_dir = os.path.join(HERE, "..", "build", "csrc")
+    build_dir = os.path.join(os.path.dirname(lib), "..", "build", "csrc") if lib == LIB else os.path.join(
+        os.path.dirname(lib), "obj")
     os.makedirs(build_dir, exist_ok=True)
     procs = []
     for src in SOURCES:
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, "-c", os.path.join(csrc, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -52,14 +55,14 @@ def build(verbose=False, force=False):
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
         if verbose and out:
             sys.stderr.write(out.decode())
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *FLAGS, "-shared", *objs, "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

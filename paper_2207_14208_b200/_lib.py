@@ -50,6 +50,7 @@ SIGNATURES = {
     "gmg_launch_count": (_i64, [_p]),
     "gmg_debug_gs_trace": (_i64, [_p, _i, _p, _i64]),
     "gmg_debug_ghost_trace": (_i64, [_p, _i, _p, _i64]),
+    "gmg_debug_gs_knobs": (_i, [_p, _p, _i]),
     "gmg_device_bytes": (_i64, [_p]),
     "gmg_profile": (_i, [_p, _i]),
     "gmg_profile_read": (_i, [_p, _i, _i, _p, _p]),
@@ -65,13 +66,20 @@ def load():
     if _lib is not None:
         return _lib
     from . import _build
-    if _build.needs_build():
-        _build.build()
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing; run __graft_entry__.build()")
-    lib = ctypes.CDLL(LIB_PATH)
+    path = os.environ.get("GMG_LIB_OVERRIDE")  # diagnostics: A/B builds (tools/build_alt.sh)
+    if not path:
+        path = LIB_PATH
+        if _build.needs_build():
+            _build.build()
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None and path != LIB_PATH:
+            continue  # an older A/B build may lack newer diagnostics
+        if fn is None:
+            raise ImportError(f"{path} does not export {name}")
         fn.restype = res
         fn.argtypes = args
     _lib = lib
@@ -207,6 +215,11 @@ class Context:
         out = np.zeros((ntasks, 24), dtype=np.int64)
         n = self.lib.gmg_debug_gs_trace(self.ctx, level, out.ctypes.data, out.size)
         return out if n else None
+
+    def gs_knobs(self, sleep_ns=None, variant=-1):
+        """Diagnostics: GS loader/writer back-off (ns x4) and variant."""
+        arr = None if sleep_ns is None else (ctypes.c_int * 4)(*sleep_ns)
+        self.check(self.lib.gmg_debug_gs_knobs(self.ctx, arr, variant))
 
     @property
     def device_bytes(self):

@@ -1136,6 +1136,12 @@ int64_t gmg_debug_gs_trace(gmg_ctx* ctx, int li, long long* host, int64_t cap) {
   GMG_CHECK(ctx, cudaMemcpy(host, l.trace, sizeof(long long) * n, cudaMemcpyDeviceToHost));
   return n;
 }
+int gmg_debug_gs_knobs(gmg_ctx* ctx, const int* sleep_ns, int variant) {
+  if (sleep_ns)
+    for (int i = 0; i < 4; ++i) ctx->gs_sleep[i] = sleep_ns[i];
+  if (variant >= 0) ctx->gs_variant = variant;
+  return 0;
+}
 int64_t gmg_device_bytes(const gmg_ctx* ctx) { return ctx->bytes; }
 
 int gmg_profile(gmg_ctx* ctx, int mask) {
