@@ -301,83 +301,90 @@ void launch_restrict_interior(const Geom& gf, const double* r_f, const Geom& gc,
 // ErrorInterpolation + correction (transfer.py:124-151, solver.py:198):
 // u += sum_c w_c e[src_c] on internal and ghost fine nodes; corner c of
 // {0,1}^D in C order, w_c = prod_k (odd_k ? 1/2 : [c_k == 0]).
-// Row loop over fine rows (grid-stride); each thread takes IC columns of the
-// row (stride blockDim) and issues all of their loads before any arithmetic,
-// so enough bytes are in flight to cover HBM latency.  The coarse rows and
-// the plane/row weights of the 2^D corners are per-row constants; only the
-// column parity varies along the row.
+// The padded fine array is walked as 16-byte pairs of positions (2m, 2m+1)
+// -- fine columns k = 2m-3 (odd) and 2m-2 (even), which share the coarse
+// columns m-2 and m-1 -- so u moves as one vector load/store and the labels
+// as one 2-byte load; each thread takes PPT pairs a grid stride apart with
+// all their loads issued before any arithmetic.  Zero-weight corners are
+// still multiplied and summed, like the reference's dense 2^D product.
+constexpr int PPT = 2;  // pairs per thread
+
 template <int D>
-__global__ void __launch_bounds__(128) interp_add_kernel(Geom gf, const uint8_t* __restrict__ lab_f,
-                                                         double* __restrict__ u, Geom gc,
-                                                         const double* __restrict__ e) {
+__global__ void __launch_bounds__(256, 4) interp_add_kernel(Geom gf, const uint8_t* __restrict__ lab_f,
+                                                            double* __restrict__ u, Geom gc,
+                                                            const double* __restrict__ e) {
   constexpr int NC = 1 << D;
+  constexpr int NR = D == 3 ? 4 : 2;  // corner rows (c0, c1)
   const int nf = (int)gf.n;
-  const int64_t nrows = D == 3 ? (int64_t)nf * nf : nf;
-  for (int64_t rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
-    const int ii = D == 3 ? (int)(rr / nf) : 0;
-    const int jj = D == 3 ? (int)(rr % nf) : (int)rr;
-    // corner rows (c0, c1) and their weights; 2-D uses c0 = 0 only
-    const double* erow[2][2];
-    double wrow[2][2];
-    {
+  const int hp = (int)(gf.P >> 1);  // pairs per row
+  const int npairs = (int)(gf.rows * hp);
+  const int stride = gridDim.x * blockDim.x;
+  for (int q0 = blockIdx.x * blockDim.x + threadIdx.x; q0 < npairs; q0 += PPT * stride) {
+    double2 uv[PPT];
+    uint16_t L2v[PPT];
+    double ea[PPT][NR], eb[PPT][NR];
+    int oij[PPT];
+    // loads: u pair, labels, coarse columns m-2 / m-1 of every corner row
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int q = min(q0 + t * stride, npairs - 1);
+      const int row = q / hp, m = q - row * hp;
+      const int ii = D == 3 ? row / nf : 0;
+      const int jj = D == 3 ? row - ii * nf : row;
+      uv[t] = reinterpret_cast<const double2*>(u)[q];
+      L2v[t] = reinterpret_cast<const uint16_t*>(lab_f)[q];
       const int oi = ii & 1, oj = jj & 1;
-      const int64_t hi = ii >> 1, hj = jj >> 1;
+      oij[t] = oi * 2 + oj;
+      const int hi = ii >> 1, hj = jj >> 1;
+      // (clamped inside the padded row for pad pairs)
+      const int cm = max(m - 2, 0) + (int)OFF, cn = max(m - 1, 0) + (int)OFF;
 #pragma unroll
-      for (int c0 = 0; c0 < 2; ++c0)
-#pragma unroll
-        for (int c1 = 0; c1 < 2; ++c1) {
-          const int64_t ri = hi + (oi ? c0 : 0), rj = hj + (oj ? c1 : 0);
-          erow[c0][c1] = e + (D == 3 ? (ri * gc.n + rj) * gc.P : rj * gc.P) + OFF;
-          const double wi = oi ? 0.5 : (c0 == 0 ? 1.0 : 0.0);
-          const double wj = oj ? 0.5 : (c1 == 0 ? 1.0 : 0.0);
-          wrow[c0][c1] = D == 3 ? (1.0 * wi) * wj : 1.0 * wj;
-        }
+      for (int r = 0; r < NR; ++r) {
+        const int c0 = D == 3 ? r >> 1 : 0, c1 = r & 1;
+        const int ri = hi + (oi ? c0 : 0), rj = hj + (oj ? c1 : 0);
+        const double* er = e + (D == 3 ? ((int64_t)ri * gc.n + rj) * gc.P : (int64_t)rj * gc.P);
+        ea[t][r] = er[cm];
+        eb[t][r] = er[cn];
+      }
     }
-    double* urow = u + rr * gf.P + OFF;
-    const uint8_t* lrow = lab_f + rr * gf.P + OFF;
-    for (int k0 = threadIdx.x; k0 < nf; k0 += IC * blockDim.x) {
-      double uv[IC], p[IC][NC];
-      uint8_t L[IC];
 #pragma unroll
-      for (int q = 0; q < IC; ++q) {
-        const int kk = k0 + q * (int)blockDim.x;
-        const bool in = kk < nf;
-        const int kc = in ? kk : 0;
-        L[q] = in ? lrow[kc] : (uint8_t)PAD;  // out of the row: never written
-        uv[q] = urow[kc];
-        const int ok = kc & 1, hk = kc >> 1, col1 = hk + ok;
-        const double wk0 = ok ? 0.5 : 1.0, wk1 = ok ? 0.5 : 0.0;
-        if (D == 3) {
+    for (int t = 0; t < PPT; ++t) {
+      const int q = q0 + t * stride;
+      if (q >= npairs) continue;
+      const uint8_t la = (uint8_t)(L2v[t] & 0xFF), lb = (uint8_t)(L2v[t] >> 8);
+      const bool wa = la == INTERNAL || la == GHOST, wb = lb == INTERNAL || lb == GHOST;
+      if (!wa && !wb) continue;
+      const int oi = oij[t] >> 1, oj = oij[t] & 1;
+      double pa[NC], pb[NC];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int c0 = c >> 2, c1 = (c >> 1) & 1, c2 = c & 1;
-            p[q][c] = (wrow[c0][c1] * (c2 ? wk1 : wk0)) * erow[c0][c1][c2 ? col1 : hk];
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int c1 = c >> 1, c2 = c & 1;
-            p[q][c] = (wrow[0][c1] * (c2 ? wk1 : wk0)) * erow[0][c1][c2 ? col1 : hk];
-          }
-        }
+      for (int r = 0; r < NR; ++r) {
+        const int c0 = D == 3 ? r >> 1 : 0, c1 = r & 1;
+        const double wi = oi ? 0.5 : (c0 == 0 ? 1.0 : 0.0);
+        const double wj = oj ? 0.5 : (c1 == 0 ? 1.0 : 0.0);
+        const double wr = D == 3 ? (1.0 * wi) * wj : 1.0 * wj;
+        // odd column k = 2m-3: hk = m-2, col1 = m-1, weights (1/2, 1/2);
+        // even column k = 2m-2: hk = col1 = m-1, weights (1, 0)
+        pa[2 * r] = (wr * 0.5) * ea[t][r];
+        pa[2 * r + 1] = (wr * 0.5) * eb[t][r];
+        pb[2 * r] = (wr * 1.0) * eb[t][r];
+        pb[2 * r + 1] = (wr * 0.0) * eb[t][r];
       }
-#pragma unroll
-      for (int q = 0; q < IC; ++q) {
-        if (L[q] != INTERNAL && L[q] != GHOST) continue;
-        urow[k0 + q * (int)blockDim.x] = uv[q] + np_sum<NC>(p[q]);
-      }
+      double2 o = uv[t];
+      if (wa) o.x = uv[t].x + np_sum<NC>(pa);
+      if (wb) o.y = uv[t].y + np_sum<NC>(pb);
+      reinterpret_cast<double2*>(u)[q] = o;
     }
   }
 }
 
 void launch_interp_add(const Geom& gf, const uint8_t* lab_f, double* u_f, const Geom& gc,
                        const double* e_c, cudaStream_t st) {
-  const int64_t nrows = gf.d == 3 ? gf.n * gf.n : gf.n;
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 16));
+  const int64_t npairs = gf.rows * (gf.P / 2);
+  const unsigned blocks = grid_for((npairs + PPT - 1) / PPT, 256, 148 * 8);
   if (gf.d == 3)
-    interp_add_kernel<3><<<blocks, 128, 0, st>>>(gf, lab_f, u_f, gc, e_c);
+    interp_add_kernel<3><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
   else
-    interp_add_kernel<2><<<blocks, 128, 0, st>>>(gf, lab_f, u_f, gc, e_c);
+    interp_add_kernel<2><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
 }
 
 // Band BFS group (transfer.py:245-246): x_i = (sum_k x[nbr_k] * mask_k) /
