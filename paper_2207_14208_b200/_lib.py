@@ -171,8 +171,11 @@ class Context:
         host = np.ascontiguousarray(host, dtype=np.float64)
         self.check(self.lib.gmg_set_vector(self.ctx, level, which, ptr(host)))
 
-    def get_vector(self, level, which, n):
-        out = np.empty(n, dtype=np.float64)
+    def get_vector(self, level, which, n, out=None):
+        if out is None:
+            out = np.empty(n, dtype=np.float64)
+        elif out.shape != (n,) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous float64 array of the vector's length")
         if n:
             self.check(self.lib.gmg_get_vector(self.ctx, level, which, ptr(out)))
         return out

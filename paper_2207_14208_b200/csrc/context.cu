@@ -91,6 +91,8 @@ struct gmg_ctx {
   void* cb_user = nullptr;
   unsigned long long* dmax = nullptr;  // reduction slots
   unsigned long long* hmax = nullptr;  // pinned mirror
+  double* stage = nullptr;             // contiguous host-layout staging for set/get_vector
+  int64_t stage_n = 0;
   std::string err;
   int64_t launches = 0;
   int64_t bytes = 0;
@@ -551,6 +553,22 @@ int cycle_level(gmg_ctx* ctx, int li) {
   return op_smooth(ctx, l, ctx->nu2);
 }
 
+// staging buffer large enough for one host-layout vector of level l
+int stage_for(gmg_ctx* ctx, const DevLevel& l) {
+  const int64_t need = l.g.n * l.g.rows;
+  if (ctx->stage_n >= need) return 0;
+  if (ctx->stage) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->stage);
+    ctx->bytes -= (int64_t)sizeof(double) * ctx->stage_n;
+    ctx->stage = nullptr;
+    ctx->stage_n = 0;
+  }
+  if (dalloc(ctx, &ctx->stage, need)) return -1;
+  ctx->stage_n = need;
+  return 0;
+}
+
 bool levels_ready(gmg_ctx* ctx) {
   for (auto& l : ctx->L)
     if (!l.ready) return false;
@@ -613,6 +631,7 @@ void gmg_destroy(gmg_ctx* ctx) {
   }
   for (auto e : ctx->pool) cudaEventDestroy(e);
   if (ctx->dmax) cudaFree(ctx->dmax);
+  if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->hmax) cudaFreeHost(ctx->hmax);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
@@ -947,8 +966,11 @@ int gmg_set_vector(gmg_ctx* ctx, int li, int which, const double* host) {
   }
   double* p = vec_ptr(l, which);
   if (!p) return fail(ctx, "unknown vector");
-  GMG_CHECK(ctx, cudaMemcpy2DAsync(p + OFF, sizeof(double) * l.g.P, host, sizeof(double) * l.g.n,
-                                   sizeof(double) * l.g.n, l.g.rows, cudaMemcpyHostToDevice, ctx->stream));
+  if (stage_for(ctx, l)) return -1;
+  GMG_CHECK(ctx, cudaMemcpyAsync(ctx->stage, host, sizeof(double) * l.g.n * l.g.rows, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+  launch_repitch(ctx->stage, p, l.g.rows, l.g.n, l.g.P, true, ctx->stream);
+  ctx->launches++;
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   return 0;
 }
@@ -967,8 +989,11 @@ int gmg_get_vector(gmg_ctx* ctx, int li, int which, double* host) {
   }
   double* p = vec_ptr(l, which);
   if (!p) return fail(ctx, "unknown vector");
-  GMG_CHECK(ctx, cudaMemcpy2DAsync(host, sizeof(double) * l.g.n, p + OFF, sizeof(double) * l.g.P,
-                                   sizeof(double) * l.g.n, l.g.rows, cudaMemcpyDeviceToHost, ctx->stream));
+  if (stage_for(ctx, l)) return -1;
+  launch_repitch(p, ctx->stage, l.g.rows, l.g.n, l.g.P, false, ctx->stream);
+  ctx->launches++;
+  GMG_CHECK(ctx, cudaMemcpyAsync(host, ctx->stage, sizeof(double) * l.g.n * l.g.rows, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   return 0;
 }

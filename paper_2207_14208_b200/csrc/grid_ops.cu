@@ -476,6 +476,30 @@ void launch_scale(double* u, int64_t n, double s, cudaStream_t st) {
   scale_kernel<<<grid_for(n, 256), 256, 0, st>>>(u, n, s);
 }
 
+// Host-layout <-> padded device layout: row r of length n sits at
+// r * n in the contiguous (host) array and at r * P + OFF on the device.
+// The host copy is one contiguous DMA into a staging buffer; these kernels
+// re-pitch on the device (a 2-D memcpy with 4 KB rows runs far below the
+// PCIe / C2C rate).
+template <bool TO_PADDED>
+__global__ void __launch_bounds__(256) repitch_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                                      int64_t rows, int64_t n, int64_t P) {
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const double* s = TO_PADDED ? src + r * n : src + r * P + OFF;
+    double* d = TO_PADDED ? dst + r * P + OFF : dst + r * n;
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) d[k] = s[k];
+  }
+}
+
+void launch_repitch(const double* src, double* dst, int64_t rows, int64_t n, int64_t P, bool to_padded,
+                    cudaStream_t st) {
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(rows, 148 * 16));
+  if (to_padded)
+    repitch_kernel<true><<<blocks, 256, 0, st>>>(src, dst, rows, n, P);
+  else
+    repitch_kernel<false><<<blocks, 256, 0, st>>>(src, dst, rows, n, P);
+}
+
 // Coarsest solve right-hand side [f_c at internal nodes; g_c in lex order].
 __global__ void gather_kernel(const int64_t* __restrict__ idx, int64_t n_int, const double* __restrict__ f,
                               const int32_t* __restrict__ ghost_slot, int64_t n_gh,

@@ -138,6 +138,16 @@ class CycleDriver:
     def _get_u(self):
         raise NotImplementedError
 
+    def _fetch_u(self, u):
+        """Copy the iterate back into the caller's array ``u`` when it is a
+        matching float64 array (the reference mutates ``u`` in place), else
+        return a new array."""
+        out = self._get_u()
+        if isinstance(u, np.ndarray) and u.shape == out.shape and u.dtype == np.float64:
+            u[...] = out
+            return u
+        return out
+
     def _run_cycle(self):
         raise NotImplementedError
 
@@ -171,7 +181,7 @@ class CycleDriver:
             self._put_u(u)
         self._run_cycle()
         if u is not None:
-            u[...] = self._get_u()
+            self._fetch_u(u)
         return u
 
     def solve(self, u=None, cycles=None, tol=0.0, seed=42):
@@ -205,11 +215,7 @@ class CycleDriver:
             if tol > 0.0 and ln_norms[-1] - ln_norms[0] < math.log(tol):
                 break
 
-        out = self._get_u()
-        if isinstance(u, np.ndarray) and u.shape == out.shape and u.dtype == np.float64:
-            u[...] = out
-        else:
-            u = out
+        u = self._fetch_u(u)
         norms = [math.exp(v) if v > -math.inf else 0.0 for v in ln_norms]
         rho_seq = [math.exp(ln_norms[i + 1] - ln_norms[i]) if ln_norms[i] > -math.inf else 0.0
                    for i in range(len(ln_norms) - 1)]

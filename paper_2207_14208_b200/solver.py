@@ -144,6 +144,15 @@ class MultigridSolver(CycleDriver):
     def _get_u(self):
         return self.ctx.get_vector(0, _lib.U, self.plans[0].n_nodes)
 
+    def _fetch_u(self, u):
+        # straight into the caller's array (one D2H copy, no host temporary)
+        n = self.plans[0].n_nodes
+        if (isinstance(u, np.ndarray) and u.shape == (n,) and u.dtype == np.float64
+                and u.flags.c_contiguous and u.flags.writeable):
+            self.ctx.get_vector(0, _lib.U, n, out=u)
+            return u
+        return super()._fetch_u(u)
+
     def _run_cycle(self):
         self.ctx.cycle(1)
 
