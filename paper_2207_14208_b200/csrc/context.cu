@@ -51,6 +51,10 @@ struct DevLevel {
   int8_t* tstep = nullptr;
   double *tabsn = nullptr, *bscratch = nullptr;
   std::vector<int64_t> bfs_off;
+  int64_t nfix = 0;                // compact transport (see launch_band_transport)
+  int64_t* bfixpos = nullptr;
+  int32_t* bnbr = nullptr;
+  double *bv0 = nullptr, *bv1 = nullptr;
   // Gauss-Seidel tasks
   int2* tasks = nullptr;
   int ntasks = 0, B1 = 1, Bn = 1, C = 1;
@@ -166,7 +170,8 @@ void free_level(DevLevel& l) {
   void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
                   l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
-                  l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off};  // ticket lives in progress
+                  l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off,
+                  l.bfixpos, l.bnbr, l.bv0, l.bv1};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -321,6 +326,11 @@ BandArgs band_args(const DevLevel& l) {
   a.step = l.tstep;
   a.absn = l.tabsn;
   a.scratch = l.bscratch;
+  a.nfix = l.nfix;
+  a.fixpos = l.bfixpos;
+  a.nbr = l.bnbr;
+  a.v0 = l.bv0;
+  a.v1 = l.bv1;
   return a;
 }
 
@@ -473,7 +483,7 @@ int op_extend(gmg_ctx* ctx, DevLevel& l, double* x) {
     ctx->launches++;
   }
   launch_band_transport(a, x, ctx->stream);
-  ctx->launches += 12;
+  ctx->launches += 8;
   return 0;
 }
 
@@ -802,6 +812,36 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     if (upload(ctx, &l.band_idx, bpos.data(), nb) || upload(ctx, &l.bfs_mask, bfs_mask, nb) ||
         upload(ctx, &l.tstep, trans_step, nb * d) || upload(ctx, &l.tabsn, trans_absn, nb * d) ||
         dalloc(ctx, &l.bscratch, nb))
+      return -1;
+    // compact transport: slot of every upwind neighbour (band slot, or a
+    // fixed slot after the band for nodes outside it)
+    std::vector<std::pair<int64_t, int32_t>> bsorted((size_t)nb);
+    for (int64_t q = 0; q < nb; ++q) bsorted[q] = {band_idx[q], (int32_t)q};
+    std::sort(bsorted.begin(), bsorted.end());
+    const int64_t hstride[3] = {d == 3 ? (N + 1) * (N + 1) : N + 1, d == 3 ? N + 1 : 1, 1};
+    std::vector<int64_t> nflat((size_t)(nb * d));
+    std::vector<int32_t> nbr((size_t)(nb * d), -1);
+    std::vector<int64_t> fixed;
+    for (int64_t q = 0; q < nb; ++q)
+      for (int k = 0; k < d; ++k) {
+        const int64_t f = band_idx[q] - (int64_t)trans_step[q * d + k] * hstride[k];
+        nflat[q * d + k] = f;
+        auto it = std::lower_bound(bsorted.begin(), bsorted.end(), std::make_pair(f, (int32_t)INT32_MIN));
+        if (it != bsorted.end() && it->first == f)
+          nbr[q * d + k] = it->second;
+        else
+          fixed.push_back(f);
+      }
+    std::sort(fixed.begin(), fixed.end());
+    fixed.erase(std::unique(fixed.begin(), fixed.end()), fixed.end());
+    for (int64_t x = 0; x < nb * d; ++x)
+      if (nbr[x] < 0)
+        nbr[x] = (int32_t)(nb + (std::lower_bound(fixed.begin(), fixed.end(), nflat[x]) - fixed.begin()));
+    l.nfix = (int64_t)fixed.size();
+    std::vector<int64_t> fpos(fixed.size());
+    for (size_t x = 0; x < fixed.size(); ++x) fpos[x] = flat_to_pos(l.g, fixed[x]);
+    if (upload(ctx, &l.bnbr, nbr.data(), nb * d) || upload(ctx, &l.bfixpos, fpos.data(), l.nfix) ||
+        dalloc(ctx, &l.bv0, nb + l.nfix) || dalloc(ctx, &l.bv1, nb + l.nfix))
       return -1;
   }
 

@@ -44,6 +44,11 @@ struct BandArgs {
   const int8_t* step;     // [nb][d] upwind step
   const double* absn;     // [nb][d]
   double* scratch;        // [nb]
+  // compact transport: slots [0, nb) band nodes, [nb, nb + nfix) fixed upwind neighbours
+  int64_t nfix;
+  const int64_t* fixpos;  // [nfix] positions of the fixed neighbours
+  const int32_t* nbr;     // [nb][d] slot of the upwind neighbour along each axis
+  double *v0, *v1;        // [nb + nfix] ping-pong values
 };
 
 void launch_gs_sweep(const GsArgs& a, int grid, cudaStream_t st);

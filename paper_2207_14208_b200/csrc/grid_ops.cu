@@ -419,37 +419,53 @@ void launch_band_bfs(const BandArgs& a, double* x, int64_t lo, int64_t hi, cudaS
     band_bfs_kernel<2><<<blocks, 256, 0, st>>>(a, x, lo, hi);
 }
 
-// One Jacobi transport step (transfer.py:249-251):
+// Jacobi transport steps (transfer.py:249-251):
 // v_i <- v_i - 0.5 * sum_k |n_k| (v_i - v[i - step_k s_k]).
-template <int D>
-__global__ void __launch_bounds__(256) band_step_kernel(BandArgs a, const double* __restrict__ x) {
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= a.nb) return;
-  const int64_t i = a.idx[q];
-  const int64_t s[3] = {a.g.s0, a.g.s1, a.g.s2};
-  const double vi = x[i];
-  double t[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) t[k] = a.absn[q * D + k] * (vi - x[i - (int64_t)a.step[q * D + k] * s[k]]);
-  a.scratch[q] = vi - 0.5 * seq_sum<D>(t);
+// The six steps run on a compact vector: slots [0, nb) hold the band nodes,
+// slots [nb, nb + nfix) the non-band upwind neighbours (constant during the
+// transport), and nbr[q][k] is the slot of node q's upwind neighbour along
+// axis k (q itself for step 0).  Gather once, ping-pong six times between
+// two L2-resident copies, scatter once -- instead of six full passes over
+// scattered grid positions.
+__global__ void band_gather_kernel(BandArgs a, const double* __restrict__ x) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= a.nb + a.nfix) return;
+  const double v = t < a.nb ? x[a.idx[t]] : x[a.fixpos[t - a.nb]];
+  a.v0[t] = v;
+  if (t >= a.nb) a.v1[t] = v;
 }
 
-__global__ void band_commit_kernel(BandArgs a, double* __restrict__ x) {
+template <int D>
+__global__ void __launch_bounds__(256) band_iter_kernel(BandArgs a, const double* __restrict__ vin,
+                                                        double* __restrict__ vout) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= a.nb) return;
-  x[a.idx[q]] = a.scratch[q];
+  const double vi = vin[q];
+  double t[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) t[k] = a.absn[q * D + k] * (vi - vin[a.nbr[q * D + k]]);
+  vout[q] = vi - 0.5 * seq_sum<D>(t);
+}
+
+__global__ void band_scatter_kernel(BandArgs a, const double* __restrict__ v, double* __restrict__ x) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q < a.nb) x[a.idx[q]] = v[q];
 }
 
 void launch_band_transport(const BandArgs& a, double* x, cudaStream_t st) {
   if (a.nb == 0) return;
   const unsigned blocks = (unsigned)((a.nb + 255) / 256);
+  const unsigned gblocks = (unsigned)((a.nb + a.nfix + 255) / 256);
+  band_gather_kernel<<<gblocks, 256, 0, st>>>(a, x);
   for (int it = 0; it < 6; ++it) {
+    const double* vin = (it & 1) ? a.v1 : a.v0;
+    double* vout = (it & 1) ? a.v0 : a.v1;
     if (a.g.d == 3)
-      band_step_kernel<3><<<blocks, 256, 0, st>>>(a, x);
+      band_iter_kernel<3><<<blocks, 256, 0, st>>>(a, vin, vout);
     else
-      band_step_kernel<2><<<blocks, 256, 0, st>>>(a, x);
-    band_commit_kernel<<<blocks, 256, 0, st>>>(a, x);
+      band_iter_kernel<2><<<blocks, 256, 0, st>>>(a, vin, vout);
   }
+  band_scatter_kernel<<<blocks, 256, 0, st>>>(a, a.v0, x);  // six steps: result back in v0
 }
 
 __global__ void abs_max_kernel(const double* __restrict__ u, int64_t n, unsigned long long* maxbits) {
