@@ -9,6 +9,7 @@
 // correction, nu2 smoothing steps.  Nothing leaves the device except the
 // coarsest right-hand side when the host SuperLU callback is used.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -287,6 +288,11 @@ Geom make_geom(int d, int64_t N, double reaction) {
   g.denom = 2.0 * d + reaction * g.h2;
   g.inv = 1.0 / g.denom;
   g.c = g.denom / g.h2;
+  {
+    int e2 = 0;
+    g.h2pow2 = std::frexp(g.h2, &e2) == 0.5 ? 1 : 0;
+    g.rh2 = 1.0 / g.h2;
+  }
   return g;
 }
 

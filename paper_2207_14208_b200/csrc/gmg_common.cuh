@@ -105,7 +105,12 @@ struct Geom {
   int64_t s0, s1, s2;  // position strides of axes 0, 1, 2 (the fastest axis has stride 1)
   int64_t nodes;       // allocated positions = rows * P
   double h2, denom, inv, c;  // h^2, 2d + reaction h^2, 1/denom, denom/h^2
+  double rh2;                // 1/h^2; exact stand-in for "/ h2" when h2 is a power of two
+  int h2pow2;                // h2 is a power of two (then x / h2 == x * rh2 bit for bit)
 };
+
+// x / h^2 as the reference computes it; a multiply when that is exact
+__device__ __forceinline__ double div_h2(const Geom& g, double x) { return g.h2pow2 ? x * g.rh2 : x / g.h2; }
 
 // position -> multi-index (m[d-1] is the fastest axis); returns false on padding
 __device__ __forceinline__ bool pos_multi(const Geom& g, int64_t pos, int64_t* m) {

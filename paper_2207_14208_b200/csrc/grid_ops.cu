@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(256) residual_interior_kernel(Geom g, const ui
     else
       s = ((u[i - g.s0] + u[i + g.s0]) + u[i - 1]) + u[i + 1];
     s = s + 0.0;
-    const double v = (f[i] - g.c * u[i]) + s / g.h2;
+    const double v = (f[i] - g.c * u[i]) + div_h2(g, s);
     r[i] = v;
     am = (__double_as_longlong(fabs(v)) > __double_as_longlong(am)) ? fabs(v) : am;
   }
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(128) residual_rows3_kernel(Geom g, const uint8
       for (int q = 0; q < IC; ++q) {
         if (L[q] != INTERNAL) continue;
         const double sv = s[q] + 0.0;
-        const double v = (fv[q] - g.c * uc[q]) + sv / g.h2;
+        const double v = (fv[q] - g.c * uc[q]) + div_h2(g, sv);
         if (WRITE) r[base + k0 + q * (int)blockDim.x] = v;
         am = (__double_as_longlong(fabs(v)) > __double_as_longlong(am)) ? fabs(v) : am;
       }
@@ -165,10 +165,171 @@ __global__ void __launch_bounds__(128) residual_rows3_kernel(Geom g, const uint8
   block_max_commit(am, maxbits);
 }
 
+// 3-D plane-marching version (production): a CTA owns RM_TJ rows x RM_TK
+// columns of every plane of its segment and walks the planes in order.  Each
+// plane's u tile (+1 halo), f tile and labels arrive by cp.async in a ring
+// of RM_S slots, RM_S - 1 planes ahead, so u is read from L2 about once
+// (+ halo) instead of once per stencil neighbour.  Same arithmetic order as
+// residual_interior_kernel.  r == nullptr: only the maximum (norm pass).
+constexpr int RM_TJ = 8, RM_TK = 64, RM_S = 5, RM_UW = RM_TK + 4;  // u row: [pad, k0-1, k0 .. k0+63, k0+64, pad]
+struct __align__(16) ResMarchSmem {
+  double u[RM_S][RM_TJ + 2][RM_UW];
+  double f[RM_S][RM_TJ][RM_TK];
+  uint8_t lab[RM_S][RM_TJ][RM_TK];
+};
+
+__device__ __forceinline__ void cpa16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cpa8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cpa4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(RM_TJ * 32) residual_march3_kernel(Geom g, const uint8_t* __restrict__ lab,
+                                                                     const double* __restrict__ u,
+                                                                     const double* __restrict__ f,
+                                                                     double* __restrict__ r,
+                                                                     unsigned long long* maxbits) {
+  extern __shared__ __align__(16) unsigned char rm_raw[];
+  ResMarchSmem& S = *reinterpret_cast<ResMarchSmem*>(rm_raw);
+  const int N = (int)g.N;
+  const int k0 = 1 + (int)blockIdx.x * RM_TK, j0 = 1 + (int)blockIdx.y * RM_TJ;
+  const int per = (N - 1 + (int)gridDim.z - 1) / (int)gridDim.z;
+  const int ib = 1 + (int)blockIdx.z * per, ie = min(N - 1, ib + per - 1);
+  if (ib > ie) return;
+  const int tid = threadIdx.x;
+  // Copy descriptors: each plane is the same set of RM_NCP copies (u rows with
+  // halo, f and label rows) shifted by a plane stride, so every thread
+  // resolves its (at most 3) copies once: shared address in slot 0, global
+  // address in plane 0, size (0 = none).
+  constexpr int UPR = RM_TK / 2 + 2, FPR = RM_TK / 2, LPR = RM_TK / 4;
+  constexpr int NU = (RM_TJ + 2) * UPR, NF = RM_TJ * FPR, NL = RM_TJ * LPR, RM_NCP = NU + NF + NL;
+  constexpr int NT = RM_TJ * 32, NQ = (RM_NCP + NT - 1) / NT;
+  unsigned dsm[NQ], dss[NQ];
+  const char* dg[NQ];
+  int64_t dps[NQ];
+  int dsz[NQ];
+  const int64_t pstride = g.n * g.P;  // elements per plane
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int x = tid + q * NT;
+    dsz[q] = 0;
+    dsm[q] = dss[q] = 0;
+    dg[q] = nullptr;
+    dps[q] = 0;
+    if (x < NU) {
+      const int jr = x / UPR, c = x - jr * UPR, j = j0 - 1 + jr;
+      int col = 0, kk = 0, sz = 0;
+      if (c < RM_TK / 2) {
+        col = 2 + 2 * c, kk = k0 + 2 * c, sz = k0 + 2 * c <= N - 1 ? 16 : 0;
+      } else if (c == RM_TK / 2) {
+        col = 1, kk = k0 - 1, sz = 8;
+      } else {
+        col = 2 + RM_TK, kk = k0 + RM_TK, sz = k0 + RM_TK <= N ? 8 : 0;
+      }
+      if (j > N) sz = 0;
+      dsz[q] = sz;
+      dsm[q] = (unsigned)__cvta_generic_to_shared(&S.u[0][jr][col]);
+      dss[q] = (unsigned)sizeof(S.u[0]);
+      dg[q] = reinterpret_cast<const char*>(u + (int64_t)j * g.P + OFF + kk);
+      dps[q] = pstride * 8;
+    } else if (x < NU + NF) {
+      const int y = x - NU, jr = y / FPR, c = y - jr * FPR, j = j0 + jr;
+      dsz[q] = (j <= N - 1 && k0 + 2 * c <= N - 1) ? 16 : 0;
+      dsm[q] = (unsigned)__cvta_generic_to_shared(&S.f[0][jr][2 * c]);
+      dss[q] = (unsigned)sizeof(S.f[0]);
+      dg[q] = reinterpret_cast<const char*>(f + (int64_t)j * g.P + OFF + k0 + 2 * c);
+      dps[q] = pstride * 8;
+    } else if (x < RM_NCP) {
+      const int y = x - NU - NF, jr = y / LPR, w = y - jr * LPR, j = j0 + jr;
+      dsz[q] = (j <= N - 1 && k0 + 4 * w <= N - 1) ? 4 : 0;
+      dsm[q] = (unsigned)__cvta_generic_to_shared(&S.lab[0][jr][4 * w]);
+      dss[q] = (unsigned)sizeof(S.lab[0]);
+      dg[q] = reinterpret_cast<const char*>(lab + (int64_t)j * g.P + OFF + k0 + 4 * w);
+      dps[q] = pstride;
+    }
+  }
+  // copy plane p into slot p mod RM_S
+  auto fetch = [&](int p) {
+    if (p <= N) {
+      const unsigned sl = (unsigned)(p % RM_S);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const unsigned dst = dsm[q] + sl * dss[q];
+        const char* src = dg[q] + (int64_t)p * dps[q];
+        if (dsz[q] == 16)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        else if (dsz[q] == 8)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+        else if (dsz[q] == 4)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+      }
+    }
+    cpa_commit();
+  };
+  // prologue: planes ib-1 .. ib+RM_S-2
+  for (int p = ib - 1; p <= ib + RM_S - 2; ++p) fetch(p);
+  const int tj = tid >> 5, lane = tid & 31;
+  const int j = j0 + tj;
+  double am = 0.0;
+  for (int i = ib; i <= ie; ++i) {
+    cpa_wait<RM_S - 3>();  // planes <= i+1 have landed
+    __syncthreads();
+    const int sm = (i - 1) % RM_S, sc = i % RM_S, sp = (i + 1) % RM_S;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int kk = lane + 32 * h, k = k0 + kk;
+      if (j > N - 1 || k > N - 1) continue;
+      if (S.lab[sc][tj][kk] != INTERNAL) continue;
+      const double um = S.u[sm][tj + 1][kk + 2], up = S.u[sp][tj + 1][kk + 2];
+      const double un = S.u[sc][tj][kk + 2], us = S.u[sc][tj + 2][kk + 2];
+      const double uw = S.u[sc][tj + 1][kk + 1], ue = S.u[sc][tj + 1][kk + 3];
+      const double uc = S.u[sc][tj + 1][kk + 2];
+      double s = ((((um + up) + un) + us) + uw) + ue;
+      s = s + 0.0;
+      const double v = (S.f[sc][tj][kk] - g.c * uc) + div_h2(g, s);
+      if (WRITE) r[((int64_t)i * g.n + j) * g.P + k + OFF] = v;
+      am = (__double_as_longlong(fabs(v)) > __double_as_longlong(am)) ? fabs(v) : am;
+    }
+    __syncthreads();  // slot of plane i-1 is refilled next
+    fetch(i + RM_S - 1);
+  }
+  cpa_wait<0>();
+  block_max_commit(am, maxbits);
+}
+
 void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,
                               const double* f, double* r, unsigned long long* maxbits,
                               cudaStream_t st) {
-  if (g.d == 3 && getenv("GMG_RES_STREAM")) {
+  if (g.d == 3 && !getenv("GMG_RES_ROWS")) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(residual_march3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ResMarchSmem));
+      cudaFuncSetAttribute(residual_march3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ResMarchSmem));
+      attr = true;
+    }
+    const int64_t tk = (g.N - 1 + RM_TK - 1) / RM_TK, tj = (g.N - 1 + RM_TJ - 1) / RM_TJ;
+    const int64_t segs = std::max<int64_t>(1, std::min<int64_t>((g.N - 1) / 4, 148 * 4 / (tk * tj)));
+    dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)segs);
+    if (r)
+      residual_march3_kernel<true><<<grid, RM_TJ * 32, sizeof(ResMarchSmem), st>>>(g, labels, u, f, r, maxbits);
+    else
+      residual_march3_kernel<false><<<grid, RM_TJ * 32, sizeof(ResMarchSmem), st>>>(g, labels, u, f, r, maxbits);
+  } else if (g.d == 3 && getenv("GMG_RES_STREAM")) {
     dim3 grid((unsigned)((g.N - 1 + RT_K - 1) / RT_K), (unsigned)((g.N - 1 + RT_J - 1) / RT_J));
     residual_stream3_kernel<<<grid, 256, 0, st>>>(g, labels, u, f, r, maxbits);
   } else if (g.d == 3) {
