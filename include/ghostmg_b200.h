@@ -54,7 +54,9 @@ enum gmg_op {
   GMG_OP_RESTRICT_GHOST = 8, /* ref transfer.py:116-121 R_EXT(l) -> G(l+1)   */
   GMG_OP_INTERP_ADD = 9,     /* ref transfer.py:149-151 + solver.py:198      */
   GMG_OP_ZERO_U = 10,
-  GMG_OP_COARSE_SOLVE = 11   /* ref solver.py:157-166 on the coarsest level */
+  GMG_OP_COARSE_SOLVE = 11,  /* ref solver.py:157-166 on the coarsest level */
+  GMG_OP_RES_RESTRICT = 12   /* 3-D: smoothing.py:111-118 fused into transfer.py:88-93,
+                                U, F(l) -> F(l+1) without materialising R_INT */
 };
 
 /* Library version (major*10000 + minor*100 + patch). */

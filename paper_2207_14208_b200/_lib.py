@@ -18,6 +18,7 @@ U, F, G, R_INT, R_EXT = 0, 1, 2, 3, 4
 OP_GS_SWEEP, OP_GHOST_SWEEP, OP_SMOOTH, OP_RES_INT, OP_RES_GHOST = 0, 1, 2, 3, 4
 OP_EXTEND_REXT, OP_EXTEND_U, OP_RESTRICT_INT, OP_RESTRICT_GHOST, OP_INTERP_ADD, OP_ZERO_U = 5, 6, 7, 8, 9, 10
 OP_COARSE_SOLVE = 11
+OP_RES_RESTRICT = 12
 KCLASS = {"gs_sweep": 0, "ghost_sweep": 1, "residual": 2, "band": 3, "restrict": 4,
           "interp": 5, "coarse": 6, "norm": 7}
 

@@ -123,6 +123,8 @@ struct gmg_ctx {
   double acc_ms[8][16] = {};       // accumulated per (class, level)
   int64_t acc_n[8][16] = {};
   // CUDA graph of one cycle (used when the coarsest solve needs no host callback)
+  bool fuse_res_restrict = false;  // 3-D fused residual + restriction (GMG_FUSE_RES=1; measured on par
+                                   // with the two separate passes at 512^3)
   bool use_graph = true;
   bool graph_valid = false;
   int graph_mask = 0;
@@ -501,6 +503,14 @@ int op_restrict_int(gmg_ctx* ctx, DevLevel& f, DevLevel& c) {
   return 0;
 }
 
+int op_res_restrict(gmg_ctx* ctx, DevLevel& f, DevLevel& c) {
+  Scope s(ctx, 4);
+  if (!c.rmask) return fail(ctx, "restriction mask missing (levels set out of order?)");
+  launch_res_restrict3(f.g, f.labels, f.u, f.f, c.g, c.rmask, c.f, ctx->stream);
+  ctx->launches++;
+  return 0;
+}
+
 int op_restrict_ghost(gmg_ctx* ctx, DevLevel& f, DevLevel& c) {
   if (c.ng == 0) return 0;
   Scope s(ctx, 4);
@@ -549,10 +559,17 @@ int cycle_level(gmg_ctx* ctx, int li) {
   DevLevel& c = ctx->L[li + 1];
   ctx->cur_level = li;
   if (op_smooth(ctx, l, ctx->nu1)) return -1;
-  if (op_res_int(ctx, l, nullptr)) return -1;
+  // 3-D: interior residual fused into the interior restriction (the fine
+  // residual array is not materialised); 2-D: the two separate passes
+  const bool fused = l.g.d == 3 && ctx->fuse_res_restrict;
+  if (fused) {
+    if (op_res_restrict(ctx, l, c)) return -1;
+  } else if (op_res_int(ctx, l, nullptr)) {
+    return -1;
+  }
   if (op_res_ghost(ctx, l, nullptr)) return -1;
   if (op_extend(ctx, l, l.rE)) return -1;
-  if (op_restrict_int(ctx, l, c)) return -1;
+  if (!fused && op_restrict_int(ctx, l, c)) return -1;
   if (op_restrict_ghost(ctx, l, c)) return -1;
   if (li + 1 == ctx->nlevels - 1) {
     ctx->cur_level = li + 1;
@@ -617,6 +634,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_MAX_TASKS")) ctx->gs_max_tasks = atoi(e);
   if (const char* e = getenv("GMG_NO_WS")) ctx->no_ws = e[0] == '1';
   if (const char* e = getenv("GMG_NO_GRAPH")) ctx->use_graph = e[0] != '1';
+  if (const char* e = getenv("GMG_FUSE_RES")) ctx->fuse_res_restrict = e[0] == '1';
   if (const char* e = getenv("GMG_GHOST_BATCHED")) ctx->ghost_batched = e[0] == '1';
   if (const char* e = getenv("GMG_GS_TRACE")) ctx->gs_trace = e[0] == '1';
   if (const char* e = getenv("GMG_GS_WS")) ctx->gs_ws = e[0] == '1';
@@ -1067,6 +1085,11 @@ int gmg_apply(gmg_ctx* ctx, int li, int op, int count) {
     case GMG_OP_RESTRICT_INT:
       if (!has_c) return fail(ctx, "no coarser level");
       rc = op_restrict_int(ctx, l, ctx->L[li + 1]);
+      break;
+    case GMG_OP_RES_RESTRICT:
+      if (!has_c) return fail(ctx, "no coarser level");
+      if (l.g.d != 3) return fail(ctx, "the fused residual + restriction is 3-D only");
+      rc = op_res_restrict(ctx, l, ctx->L[li + 1]);
       break;
     case GMG_OP_RESTRICT_GHOST:
       if (!has_c) return fail(ctx, "no coarser level");

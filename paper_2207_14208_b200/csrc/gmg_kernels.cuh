@@ -82,6 +82,8 @@ void launch_band_bfs(const BandArgs& a, double* x, int64_t lo, int64_t hi, cudaS
 void launch_band_transport(const BandArgs& a, double* x, cudaStream_t st);
 void launch_restrict_interior(const Geom& gf, const double* r_f, const Geom& gc, const uint32_t* rmask,
                               double* f_c, cudaStream_t st);
+void launch_res_restrict3(const Geom& gf, const uint8_t* labels, const double* u, const double* f, const Geom& gc,
+                          const uint32_t* rmask, double* f_c, cudaStream_t st);
 void launch_restrict_mask(const Geom& gf, const uint8_t* lab_f, const Geom& gc, const uint8_t* lab_c,
                           uint32_t* rmask, cudaStream_t st);
 void launch_restrict_ghost(const Geom& gf, const uint8_t* lab_f, const double* r_ext,

@@ -437,8 +437,9 @@ __global__ void __launch_bounds__(256, 3) restrict_interior_kernel(Geom gf, cons
       for (int e = 0; e < M; ++e) p[e] = rc[block_off<D>(gf, e)];
       if (m & RM_MIXED) {
         const double dc = (double)__popc(m & ((1u << M) - 1u));
+        const double w1 = 1.0 / dc;
 #pragma unroll
-        for (int e = 0; e < M; ++e) p[e] = (((m >> e) & 1u) ? 1.0 : 0.0) / dc * p[e];
+        for (int e = 0; e < M; ++e) p[e] = (((m >> e) & 1u) ? w1 : 0.0) * p[e];  // == (bit ? 1 : 0) / dc * p
       } else {
 #pragma unroll
         for (int e = 0; e < M; ++e) p[e] = fw_w<D>(e) * p[e];
@@ -446,6 +447,212 @@ __global__ void __launch_bounds__(256, 3) restrict_interior_kernel(Geom gf, cons
       f_c[ic] = np_sum<M>(p);
     }
   }
+}
+
+// Fused interior residual + interior restriction (3-D):
+// residual_internal (smoothing.py:111-118) evaluated tile by tile and fed
+// straight into InteriorRestriction.apply (transfer.py:88-93); the fine
+// residual never goes to HBM (nothing else reads it).  A CTA owns FR_TKc x
+// FR_TJc coarse nodes of every coarse plane of its segment and marches the
+// fine planes 2Ib-1 .. 2Ie+1: u (+1 halo), f and labels of fine plane p
+// arrive by cp.async in a ring of FR_S slots; the residual of each fine
+// plane is kept in a 3-plane ring; after every odd fine plane 2I+1 the
+// coarse plane I is restricted from that ring.  Non-internal fine nodes
+// carry residual 0, as in the full residual array of the unfused path.
+constexpr int FR_TJc = 4, FR_TKc = 32, FR_S = 6;
+constexpr int FRJ = 2 * FR_TJc + 1, FRK = 2 * FR_TKc + 1;  // fine residual tile 9 x 65
+constexpr int FRUJ = FRJ + 2, FRUW = 70, FRFW = 66, FRLW = 68;
+struct __align__(16) FusedSmem {
+  double u[FR_S][FRUJ][FRUW];  // column k0f-1+c at index c+1 (k0f at index 2: 16-byte aligned)
+  double f[FR_S][FRJ][FRFW];   // column k0f+c at index c
+  uint8_t lab[FR_S][FRJ][FRLW];
+  double r[3][FRJ][FRFW];
+};
+
+__global__ void __launch_bounds__(256, 2) res_restrict3_kernel(Geom g, const uint8_t* __restrict__ lab,
+                                                               const double* __restrict__ u,
+                                                               const double* __restrict__ f, Geom gc,
+                                                               const uint32_t* __restrict__ rmask,
+                                                               double* __restrict__ f_c) {
+  extern __shared__ __align__(16) unsigned char fr_raw[];
+  FusedSmem& S = *reinterpret_cast<FusedSmem*>(fr_raw);
+  const int N = (int)g.N, nc = (int)gc.n, innc = nc - 2;
+  const int K0c = 1 + (int)blockIdx.x * FR_TKc, J0c = 1 + (int)blockIdx.y * FR_TJc;
+  const int k0f = 2 * K0c - 1, j0f = 2 * J0c - 1;
+  const int per = (innc + (int)gridDim.z - 1) / (int)gridDim.z;
+  const int Ib = 1 + (int)blockIdx.z * per, Ie = min(innc, Ib + per - 1);
+  if (Ib > Ie) return;
+  const int tid = threadIdx.x;
+  // copy descriptors (see residual_march3_kernel): u rows j0f-1 .. j0f+9 with
+  // columns k0f-1 .. k0f+65, f / label rows j0f .. j0f+8 with columns k0f .. k0f+64
+  constexpr int UPR = FR_TKc + 3, FPR = FR_TKc + 1, LPR = FR_TKc / 2 + 1;
+  constexpr int NU = FRUJ * UPR, NF = FRJ * FPR, NL = FRJ * LPR, NCP = NU + NF + NL;
+  constexpr int NQ = (NCP + 255) / 256;
+  unsigned dsm[NQ], dss[NQ];
+  const char* dg[NQ];
+  int64_t dps[NQ];
+  int dsz[NQ];
+  const int64_t pstride = g.n * g.P;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int x = tid + q * 256;
+    dsz[q] = 0;
+    dsm[q] = dss[q] = 0;
+    dg[q] = nullptr;
+    dps[q] = 0;
+    if (x < NU) {
+      const int jr = x / UPR, c = x - jr * UPR, j = j0f - 1 + jr;
+      int idx, k, sz;
+      if (c < FR_TKc) {
+        k = k0f + 2 * c, idx = 2 + 2 * c, sz = k + 1 <= N ? 16 : (k <= N ? 8 : 0);
+      } else {
+        const int e = c - FR_TKc;  // 0: k0f-1, 1: k0f+64, 2: k0f+65
+        k = e == 0 ? k0f - 1 : k0f + 63 + e, idx = e == 0 ? 1 : 65 + e, sz = k <= N ? 8 : 0;
+      }
+      if (j > N) sz = 0;
+      dsz[q] = sz;
+      dsm[q] = (unsigned)__cvta_generic_to_shared(&S.u[0][jr][idx]);
+      dss[q] = (unsigned)sizeof(S.u[0]);
+      dg[q] = reinterpret_cast<const char*>(u + (int64_t)j * g.P + OFF + k);
+      dps[q] = pstride * 8;
+    } else if (x < NU + NF) {
+      const int y = x - NU, jr = y / FPR, c = y - jr * FPR, j = j0f + jr;
+      const int k = k0f + 2 * c;
+      int sz = c < FR_TKc ? (k + 1 <= N ? 16 : (k <= N ? 8 : 0)) : (k <= N ? 8 : 0);
+      if (j > N) sz = 0;
+      dsz[q] = sz;
+      dsm[q] = (unsigned)__cvta_generic_to_shared(&S.f[0][jr][2 * c]);
+      dss[q] = (unsigned)sizeof(S.f[0]);
+      dg[q] = reinterpret_cast<const char*>(f + (int64_t)j * g.P + OFF + k);
+      dps[q] = pstride * 8;
+    } else if (x < NCP) {
+      const int y = x - NU - NF, jr = y / LPR, w = y - jr * LPR, j = j0f + jr;
+      const int k = k0f + 4 * w;
+      dsz[q] = (j <= N && k <= N) ? 4 : 0;  // the last word may run into the padding: in the row
+      dsm[q] = (unsigned)__cvta_generic_to_shared(&S.lab[0][jr][4 * w]);
+      dss[q] = (unsigned)sizeof(S.lab[0]);
+      dg[q] = reinterpret_cast<const char*>(lab + (int64_t)j * g.P + OFF + k);
+      dps[q] = pstride;
+    }
+  }
+  auto fetch = [&](int p) {
+    if (p <= N) {
+      const unsigned sl = (unsigned)(p % FR_S);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const unsigned dst = dsm[q] + sl * dss[q];
+        const char* src = dg[q] + (int64_t)p * dps[q];
+        if (dsz[q] == 16)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        else if (dsz[q] == 8)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+        else if (dsz[q] == 4)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+      }
+    }
+    cpa_commit();
+  };
+  const int i0 = 2 * Ib - 1, i1 = 2 * Ie + 1;
+  for (int p = i0 - 1; p <= i0 + FR_S - 2; ++p) fetch(p);
+  // this thread's fine nodes of the residual tile (fixed across planes):
+  // element offsets of u (centre), f / r, and the label byte; -1 = none
+  constexpr int NR = (FRJ * FRK + 255) / 256;
+  int ou[NR], of[NR], ol[NR];
+  bool act[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    const int x = tid + 256 * q;
+    const int jr = x / FRK, kc = x - jr * FRK;
+    act[q] = x < FRJ * FRK;
+    ou[q] = (jr + 1) * FRUW + kc + 2;
+    of[q] = jr * FRFW + kc;
+    ol[q] = jr * FRLW + kc;
+    if (act[q] && !(j0f + jr <= N - 1 && k0f + kc <= N - 1)) ol[q] = -1;  // never internal
+  }
+  // this thread's coarse node (threads < 128)
+  const int tk = tid % FR_TKc, tj = tid / FR_TKc;
+  const int K = K0c + tk, J = J0c + tj;
+  const bool cmine = tid < FR_TKc * FR_TJc && K <= nc - 2 && J <= nc - 2;
+  const int rbase = 2 * tj * FRFW + 2 * tk;
+  const double c = g.c;
+  // restriction mask of the coarse plane restricted after the next odd fine
+  // plane, loaded a residual phase ahead
+  auto mask_of = [&](int I) -> uint32_t {
+    return (cmine && I <= Ie) ? rmask[((int64_t)I * nc + J) * gc.P + K + OFF] : 0u;
+  };
+  uint32_t mnext = mask_of(Ib);
+  for (int i = i0; i <= i1; ++i) {
+    cpa_wait<FR_S - 3>();  // u planes <= i+1, f / labels of plane i have landed
+    __syncthreads();
+    // fine residual of plane i on the 9 x 65 tile (0 off the internal nodes)
+    {
+      const double* um_ = &S.u[(i - 1) % FR_S][0][0];
+      const double* uc_ = &S.u[i % FR_S][0][0];
+      const double* up_ = &S.u[(i + 1) % FR_S][0][0];
+      const double* f_ = &S.f[i % FR_S][0][0];
+      const uint8_t* l_ = &S.lab[i % FR_S][0][0];
+      double* r_ = &S.r[i % 3][0][0];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        if (!act[q]) continue;
+        double v = 0.0;
+        if (ol[q] >= 0 && l_[ol[q]] == INTERNAL) {
+          const int o = ou[q];
+          double sum = ((((um_[o] + up_[o]) + uc_[o - FRUW]) + uc_[o + FRUW]) + uc_[o - 1]) + uc_[o + 1];
+          sum = sum + 0.0;
+          v = (f_[of[q]] - c * uc_[o]) + div_h2(g, sum);
+        }
+        r_[of[q]] = v;
+      }
+    }
+    __syncthreads();
+    fetch(i + FR_S - 1);  // into the slot of plane i-1, read for the last time above
+    if ((i & 1) && i >= i0 + 2 && cmine) {
+      // coarse plane I = (i-1)/2 from fine planes i-2, i-1, i
+      const int I = (i - 1) >> 1;
+      const int64_t ic = ((int64_t)I * nc + J) * gc.P + K + OFF;
+      const uint32_t m = mnext;
+      mnext = mask_of(I + 1);
+      if (m & RM_COARSE) {
+        const double* ra = &S.r[(i - 2) % 3][0][0] + rbase;
+        const double* rb = &S.r[(i - 1) % 3][0][0] + rbase;
+        const double* rc = &S.r[i % 3][0][0] + rbase;
+        double p[27];
+#pragma unroll
+        for (int e = 0; e < 27; ++e) {
+          const double* rp = e < 9 ? ra : (e < 18 ? rb : rc);
+          p[e] = rp[((e / 3) % 3) * FRFW + e % 3];
+        }
+        if (m & RM_MIXED) {
+          const double dc = (double)__popc(m & ((1u << 27) - 1u));
+          const double w1 = 1.0 / dc;
+#pragma unroll
+          for (int e = 0; e < 27; ++e) p[e] = (((m >> e) & 1u) ? w1 : 0.0) * p[e];  // == (bit ? 1 : 0) / dc * p
+        } else {
+#pragma unroll
+          for (int e = 0; e < 27; ++e) p[e] = fw_w<3>(e) * p[e];
+        }
+        f_c[ic] = np_sum<27>(p);
+      }
+    }
+  }
+  cpa_wait<0>();
+}
+
+void launch_res_restrict3(const Geom& gf, const uint8_t* labels, const double* u, const double* f, const Geom& gc,
+                          const uint32_t* rmask, double* f_c, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(res_restrict3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FusedSmem));
+    attr = true;
+  }
+  const int64_t innc = gc.n - 2;
+  if (innc <= 0) return;
+  const int64_t tx = (innc + FR_TKc - 1) / FR_TKc, ty = (innc + FR_TJc - 1) / FR_TJc;
+  const int64_t slots = 148 * 2;
+  const int64_t segs = std::max<int64_t>(1, std::min<int64_t>(innc / 4, (6 * slots + tx * ty - 1) / (tx * ty)));
+  dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)segs);
+  res_restrict3_kernel<<<grid, 256, sizeof(FusedSmem), st>>>(gf, labels, u, f, gc, rmask, f_c);
 }
 
 void launch_restrict_interior(const Geom& gf, const double* r_f, const Geom& gc, const uint32_t* rmask,

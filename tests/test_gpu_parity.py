@@ -59,6 +59,11 @@ def device_op_digests(ctx, plans, level, seed):
         ctx.set_vector(L + 1, _lib.F, np.zeros(c.n_nodes))
         ctx.set_vector(L, _lib.R_INT, r)
         out["restrict_int"] = GU.digest(run(_lib.OP_RESTRICT_INT, {}, (L + 1, _lib.F, c.n_nodes)))
+        if p.d == 3:
+            # fused residual + restriction (the cycle's 3-D path) must give the same coarse f
+            out["restrict_int_fused"] = GU.digest(run(
+                _lib.OP_RES_RESTRICT, {(L, _lib.U): inp["u"], (L, _lib.F): inp["f"],
+                                       (L + 1, _lib.F): np.zeros(c.n_nodes)}, (L + 1, _lib.F, c.n_nodes)))
         ctx.set_vector(L, _lib.R_EXT, inp["r_ghost"])
         ctx.apply(L, _lib.OP_EXTEND_REXT)
         if c.n_ghosts:
@@ -81,6 +86,8 @@ def test_device_ops_match_reference(name, gpu_available):
         seed, level = map(int, key.split(":"))
         got = device_op_digests(ctx, plans, level, seed)
         bad = {k: (got[k], want[k]) for k in got if k in want and got[k] != want[k]}
+        if "restrict_int_fused" in got and got["restrict_int_fused"] != want["restrict_int"]:
+            bad["restrict_int_fused"] = (got["restrict_int_fused"], want["restrict_int"])
         assert not bad, (name, key, bad)
     ctx.close()
 

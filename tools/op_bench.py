@@ -33,7 +33,7 @@ PEAK = 6540.2
 OPS = [("gs", _lib.OP_GS_SWEEP, "gs_sweep"), ("ghost", _lib.OP_GHOST_SWEEP, "ghost_sweep"),
        ("res_int", _lib.OP_RES_INT, "residual"), ("res_ghost", _lib.OP_RES_GHOST, "residual"),
        ("extend_rext", _lib.OP_EXTEND_REXT, "band"), ("restrict_int", _lib.OP_RESTRICT_INT, "restrict"),
-       ("restrict_ghost", _lib.OP_RESTRICT_GHOST, "restrict"), ("interp", _lib.OP_INTERP_ADD, "interp"),
+       ("restrict_ghost", _lib.OP_RESTRICT_GHOST, "restrict"), ("res_restrict", _lib.OP_RES_RESTRICT, "restrict"), ("interp", _lib.OP_INTERP_ADD, "interp"),
        ("extend_u", _lib.OP_EXTEND_U, "band")]
 
 
@@ -43,7 +43,7 @@ def alg_bytes(op, i):
     nI, nG, nB = p.n_internal, p.n_ghosts, p.n_band
     nIc = plans[i + 1].n_internal if i + 1 < len(plans) else 0
     return {"gs": 24 * nI, "ghost": nG * (8 * m + 40), "res_int": 24 * nI, "res_ghost": nG * (8 * m + 24),
-            "extend_rext": nB * (8 * (2 * d + 1) + 6 * 8 * (3 * d + 2)), "restrict_int": 8 * nI + 8 * nIc,
+            "extend_rext": nB * (8 * (2 * d + 1) + 6 * 8 * (3 * d + 2)), "restrict_int": 8 * nI + 8 * nIc, "res_restrict": 16 * nI + 8 * nIc,
             "restrict_ghost": 0, "interp": 16 * (nI + nG) + 8 * nIc,
             "extend_u": nB * (8 * (2 * d + 1) + 6 * 8 * (3 * d + 2))}[op]
 
