@@ -23,9 +23,11 @@ __device__ __forceinline__ int64_t block_offset(const Geom& g, int j) {
 // One batch of the ghost sweep (reference smoothing.py:135-142):
 // u_G += dtau * (g - ddot(w, u[block])).  No ghost of a batch reads another
 // ghost of the same batch, so the batch is one parallel step.
+__device__ __forceinline__ void st_pair(double* p, double v);
+
 template <int D>
 __global__ void __launch_bounds__(256) ghost_batch_kernel(GhostArgs a, double* __restrict__ u,
-                                                          int64_t lo, int64_t hi) {
+                                                          int64_t lo, int64_t hi, double* pair) {
   constexpr int M = D == 3 ? 27 : 9;
   const int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= hi) return;
@@ -39,7 +41,9 @@ __global__ void __launch_bounds__(256) ghost_batch_kernel(GhostArgs a, double* _
     y[j] = u[base + block_offset<D>(a.g, j)];
   }
   const double dot = blas_ddot<M>(x, y);
-  u[node] = u[node] + a.dtau[s] * (a.gval[s] - dot);
+  const double nv = u[node] + a.dtau[s] * (a.gval[s] - dot);
+  u[node] = nv;
+  if (pair) st_pair(pair + 2 * s, nv);  // for DAG-ordered successors (ghost_persistent_kernel)
 }
 
 // (value, done tag) pairs: written with one 16-byte store, read with one
@@ -79,14 +83,24 @@ __global__ void __launch_bounds__(256) ghost_persistent_kernel(GhostArgs a, doub
                                                                const int32_t* __restrict__ dep,
                                                                const uint32_t* __restrict__ vmask,
                                                                double* pair, int* cursor, int backoff,
-                                                               long long* gtrace) {
+                                                               long long* gtrace, int stride, int chunk0) {
   constexpr int M = D == 3 ? 27 : 9;
   const int lane = threadIdx.x & 31;
   const int64_t nchunks = a.ng / 32;
-  for (;;) {
+  // stride > 0: every warp of the (fully co-resident) grid takes chunks
+  // gw, gw + stride, ... in order -- the lowest unfinished chunk always has
+  // its dependencies done and its warp free, so this cannot deadlock, and no
+  // shared claim counter serialises the wide first batches.  stride == 0:
+  // chunks claimed in slot order through the cursor.
+  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  for (int it = 0;; ++it) {
     int chunk = 0;
-    if (lane == 0) chunk = atomicAdd(cursor, 1);
-    chunk = __shfl_sync(0xffffffffu, chunk, 0);
+    if (stride > 0) {
+      chunk = chunk0 + gw + it * stride;
+    } else {
+      if (lane == 0) chunk = chunk0 + atomicAdd(cursor, 1);
+      chunk = __shfl_sync(0xffffffffu, chunk, 0);
+    }
     if (chunk >= nchunks) return;
     const int64_t s = (int64_t)chunk * 32 + lane;
     const int64_t node = a.node[s];
@@ -215,26 +229,42 @@ void launch_ghost_levels(const GhostArgs& a, double* u, const int64_t* boff, int
 
 void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_off, const int32_t* dep,
                              const uint32_t* vmask, double* pair, int* cursor, int sms, int blocks_per_sm,
-                             int backoff, long long* gtrace, cudaStream_t st) {
-  const int64_t warps = a.ng / 32;
-  int blocks = (int)std::min<int64_t>((warps + 7) / 8, (int64_t)sms * blocks_per_sm);
+                             int backoff, long long* gtrace, bool static_chunks, int64_t slot0,
+                             cudaStream_t st) {
+  const int64_t warps = (a.ng - slot0) / 32;
+  if (warps <= 0) return;
+  // co-resident CTAs per SM (the static chunk assignment relies on it)
+  static int occ[2] = {0, 0};
+  int& o = occ[a.g.d == 3 ? 1 : 0];
+  if (o == 0) {
+    if (a.g.d == 3)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ghost_persistent_kernel<3>, 256, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ghost_persistent_kernel<2>, 256, 0);
+    if (o < 1) o = 1;
+  }
+  const int per_sm = std::min(blocks_per_sm, o);
+  int blocks = (int)std::min<int64_t>((warps + 7) / 8, (int64_t)sms * per_sm);
   if (blocks < 1) blocks = 1;
+  const int stride = static_chunks ? blocks * 8 : 0;
   if (a.g.d == 3)
-    ghost_persistent_kernel<3><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace);
+    ghost_persistent_kernel<3><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace,
+                                                       stride, (int)(slot0 / 32));
   else
-    ghost_persistent_kernel<2><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace);
+    ghost_persistent_kernel<2><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace,
+                                                       stride, (int)(slot0 / 32));
 }
 
 
 
-void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st) {
+void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, double* pair, cudaStream_t st) {
   if (hi <= lo) return;
   const int threads = 256;
   const int64_t blocks = (hi - lo + threads - 1) / threads;
   if (a.g.d == 3)
-    ghost_batch_kernel<3><<<(unsigned)blocks, threads, 0, st>>>(a, u, lo, hi);
+    ghost_batch_kernel<3><<<(unsigned)blocks, threads, 0, st>>>(a, u, lo, hi, pair);
   else
-    ghost_batch_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(a, u, lo, hi);
+    ghost_batch_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(a, u, lo, hi, pair);
 }
 
 __device__ __forceinline__ void block_max_commit(double v, unsigned long long* maxbits) {
@@ -342,9 +372,12 @@ __global__ void __launch_bounds__(256) restrict_ghost_kernel(Geom gf, const uint
     w[e] = fw_entry<D>(e) * (keep ? 1.0 : 0.0);
   }
   const double sum = np_sum<M>(w);
+  // every w[e] is 0 or a power of two (products of 1/4, 1/2, 1/4), so
+  // w[e] / sum == w[e] * (1 / sum) exactly: one division per ghost
+  const double rs = 1.0 / sum;
   double p[M];
 #pragma unroll
-  for (int e = 0; e < M; ++e) p[e] = (w[e] / sum) * r_ext[blk[e]];
+  for (int e = 0; e < M; ++e) p[e] = (w[e] * rs) * r_ext[blk[e]];
   gval_c[s] = np_sum<M>(p);
 }
 

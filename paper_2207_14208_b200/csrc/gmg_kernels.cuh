@@ -66,13 +66,14 @@ void launch_gs_diag(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t 
 size_t gs_diag_smem();
 void configure_gs_kernels();  // set max dynamic shared memory of the GS / GEMV kernels
 
-void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, cudaStream_t st);
+void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, double* pair, cudaStream_t st);
 void launch_ghost_levels(const GhostArgs& a, double* u, const int64_t* boff, int nbatch, const int32_t* dep_off,
                          const int32_t* dep, const uint32_t* vmask, double* pair, int* counter, int sms,
                          cudaStream_t st);
 void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_off, const int32_t* dep,
                              const uint32_t* vmask, double* pair, int* cursor, int sms, int blocks_per_sm,
-                             int backoff, long long* gtrace, cudaStream_t st);
+                             int backoff, long long* gtrace, bool static_chunks, int64_t slot0,
+                             cudaStream_t st);
 void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,
                            unsigned long long* maxbits, cudaStream_t st);
 void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,
