@@ -110,9 +110,6 @@ struct gmg_ctx {
   bool gs_ws = false;          // use the older TMA-ring GS kernel (GMG_GS_WS=1)
   int gs_variant = 0;          // GS implementation variant (GMG_GS_VARIANT, experiments)
   int ghost_bps = 8;           // ghost sweep: CTAs per SM (GMG_GHOST_BPS)
-  bool ghost_static = false;   // ghost sweep: static chunk assignment (GMG_GHOST_STATIC=1) instead of the claim counter
-  int64_t ghost_wide = INT64_MAX;  // ghost sweep: leading batches at least this wide run as plain launches
-                                  // (GMG_GHOST_WIDE; off: the DAG overlap across batches wins)
   bool ghost_levels = false;   // ghost sweep: level-synchronous kernel (GMG_GHOST_LEVELS=1; slower)
   int ghost_backoff = 300;     // ghost sweep: poll back-off ns (GMG_GHOST_BACKOFF)
   int gs_sleep[4] = {500, 500, 20, 200};  // GS loader / writer back-off (ns), GMG_GS_SLEEP=u,f,h,w  // one launch per ghost batch instead of the persistent sweep
@@ -456,21 +453,9 @@ int op_ghost_sweep(gmg_ctx* ctx, DevLevel& l) {
     if (!l.ghtrace && dalloc(ctx, &l.ghtrace, 3 * l.nslots)) return -1;
     gtrace = l.ghtrace;
   }
-  // wide leading batches: one fully parallel launch each (high occupancy;
-  // they also publish the (value, tag) pairs); the narrow DAG tail: one
-  // dependency-ordered persistent launch
-  int wide = 0;
-  if (!gtrace)
-    while (wide < nb && l.batch_off[wide + 1] - l.batch_off[wide] >= ctx->ghost_wide) ++wide;
-  for (int b = 0; b < wide; ++b) {
-    launch_ghost_batch(a, l.u, l.batch_off[b], l.batch_off[b + 1], l.gpair, ctx->stream);
-    ctx->launches++;
-  }
-  if (wide < nb) {
-    launch_ghost_persistent(a, l.u, l.dep_off, l.dep, l.vmask, l.gpair, l.gctr, ctx->sms, ctx->ghost_bps,
-                            ctx->ghost_backoff, gtrace, ctx->ghost_static, l.batch_off[wide], ctx->stream);
-    ctx->launches++;
-  }
+  launch_ghost_persistent(a, l.u, l.dep_off, l.dep, l.vmask, l.gpair, l.gctr, ctx->sms, ctx->ghost_bps,
+                          ctx->ghost_backoff, gtrace, ctx->stream);
+  ctx->launches++;
   return 0;
 }
 
@@ -655,8 +640,6 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_WS")) ctx->gs_ws = e[0] == '1';
   if (const char* e = getenv("GMG_GS_VARIANT")) ctx->gs_variant = atoi(e);
   if (const char* e = getenv("GMG_GHOST_BPS")) ctx->ghost_bps = std::max(1, atoi(e));
-  if (const char* e = getenv("GMG_GHOST_STATIC")) ctx->ghost_static = e[0] == '1';
-  if (const char* e = getenv("GMG_GHOST_WIDE")) ctx->ghost_wide = atoll(e);
   if (const char* e = getenv("GMG_GHOST_LEVELS")) ctx->ghost_levels = e[0] == '1';
   if (const char* e = getenv("GMG_GHOST_BACKOFF")) ctx->ghost_backoff = atoi(e);
   if (const char* e = getenv("GMG_GS_SLEEP"))

@@ -83,24 +83,14 @@ __global__ void __launch_bounds__(256) ghost_persistent_kernel(GhostArgs a, doub
                                                                const int32_t* __restrict__ dep,
                                                                const uint32_t* __restrict__ vmask,
                                                                double* pair, int* cursor, int backoff,
-                                                               long long* gtrace, int stride, int chunk0) {
+                                                               long long* gtrace) {
   constexpr int M = D == 3 ? 27 : 9;
   const int lane = threadIdx.x & 31;
   const int64_t nchunks = a.ng / 32;
-  // stride > 0: every warp of the (fully co-resident) grid takes chunks
-  // gw, gw + stride, ... in order -- the lowest unfinished chunk always has
-  // its dependencies done and its warp free, so this cannot deadlock, and no
-  // shared claim counter serialises the wide first batches.  stride == 0:
-  // chunks claimed in slot order through the cursor.
-  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  for (int it = 0;; ++it) {
+  for (;;) {
     int chunk = 0;
-    if (stride > 0) {
-      chunk = chunk0 + gw + it * stride;
-    } else {
-      if (lane == 0) chunk = chunk0 + atomicAdd(cursor, 1);
-      chunk = __shfl_sync(0xffffffffu, chunk, 0);
-    }
+    if (lane == 0) chunk = atomicAdd(cursor, 1);
+    chunk = __shfl_sync(0xffffffffu, chunk, 0);
     if (chunk >= nchunks) return;
     const int64_t s = (int64_t)chunk * 32 + lane;
     const int64_t node = a.node[s];
@@ -229,30 +219,14 @@ void launch_ghost_levels(const GhostArgs& a, double* u, const int64_t* boff, int
 
 void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_off, const int32_t* dep,
                              const uint32_t* vmask, double* pair, int* cursor, int sms, int blocks_per_sm,
-                             int backoff, long long* gtrace, bool static_chunks, int64_t slot0,
-                             cudaStream_t st) {
-  const int64_t warps = (a.ng - slot0) / 32;
-  if (warps <= 0) return;
-  // co-resident CTAs per SM (the static chunk assignment relies on it)
-  static int occ[2] = {0, 0};
-  int& o = occ[a.g.d == 3 ? 1 : 0];
-  if (o == 0) {
-    if (a.g.d == 3)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ghost_persistent_kernel<3>, 256, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ghost_persistent_kernel<2>, 256, 0);
-    if (o < 1) o = 1;
-  }
-  const int per_sm = std::min(blocks_per_sm, o);
-  int blocks = (int)std::min<int64_t>((warps + 7) / 8, (int64_t)sms * per_sm);
+                             int backoff, long long* gtrace, cudaStream_t st) {
+  const int64_t warps = a.ng / 32;
+  int blocks = (int)std::min<int64_t>((warps + 7) / 8, (int64_t)sms * blocks_per_sm);
   if (blocks < 1) blocks = 1;
-  const int stride = static_chunks ? blocks * 8 : 0;
   if (a.g.d == 3)
-    ghost_persistent_kernel<3><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace,
-                                                       stride, (int)(slot0 / 32));
+    ghost_persistent_kernel<3><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace);
   else
-    ghost_persistent_kernel<2><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace,
-                                                       stride, (int)(slot0 / 32));
+    ghost_persistent_kernel<2><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace);
 }
 
 
