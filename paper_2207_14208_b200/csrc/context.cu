@@ -109,6 +109,7 @@ struct gmg_ctx {
   bool gs_trace = false;       // record the GS task timeline (GMG_GS_TRACE=1)
   bool gs_ws = false;          // use the older TMA-ring GS kernel (GMG_GS_WS=1)
   int gs_variant = 0;          // GS implementation variant (GMG_GS_VARIANT, experiments)
+  int halo_multi = -1;         // GS halo loader: -1 by level size, 0 two-batch, 1 multi-batch (GMG_GS_HALO)
   int ghost_bps = 8;           // ghost sweep: CTAs per SM (GMG_GHOST_BPS)
   bool ghost_levels = false;   // ghost sweep: level-synchronous kernel (GMG_GHOST_LEVELS=1; slower)
   int ghost_backoff = 300;     // ghost sweep: poll back-off ns (GMG_GHOST_BACKOFF)
@@ -410,6 +411,7 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
   a.trace = nullptr;
   a.variant = ctx->gs_variant;
   for (int i = 0; i < 4; ++i) a.sleep_ns[i] = ctx->gs_sleep[i];
+  a.halo_multi = ctx->halo_multi >= 0 ? ctx->halo_multi : (l.ntasks <= 2 * ctx->sms ? 1 : 0);
   if (ctx->gs_trace && (l.ws_gs || l.diag_gs)) {
     if (!l.trace && dalloc(ctx, &l.trace, (int64_t)l.ntasks * 24)) return -1;
     GMG_CHECK(ctx, cudaMemsetAsync(l.trace, 0, sizeof(long long) * (size_t)l.ntasks * 24, ctx->stream));
@@ -639,6 +641,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_TRACE")) ctx->gs_trace = e[0] == '1';
   if (const char* e = getenv("GMG_GS_WS")) ctx->gs_ws = e[0] == '1';
   if (const char* e = getenv("GMG_GS_VARIANT")) ctx->gs_variant = atoi(e);
+  if (const char* e = getenv("GMG_GS_HALO")) ctx->halo_multi = atoi(e);
   if (const char* e = getenv("GMG_GHOST_BPS")) ctx->ghost_bps = std::max(1, atoi(e));
   if (const char* e = getenv("GMG_GHOST_LEVELS")) ctx->ghost_levels = e[0] == '1';
   if (const char* e = getenv("GMG_GHOST_BACKOFF")) ctx->ghost_backoff = atoi(e);

@@ -22,6 +22,8 @@ struct GsArgs {
   long long* trace;       // diagnostics: [ntasks][16] timeline per task, or null
   int variant;            // diagnostics: GS implementation variant (GMG_GS_VARIANT)
   int sleep_ns[4];        // back-off of the u / f / halo loaders and the writer when idle
+  int halo_multi;         // gs_diag: halo loader issues up to 4 ready batches per poll (levels with
+                          // at most ~1 task per SM; the 2-batch loader is faster when 4 share an SM)
 };
 
 // Ghost rows of one level, stored in sweep-slot order (batch, then lex).

@@ -603,93 +603,198 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         (void)leadF;
       }
     } else if (warp == 2) {
-      // ============================ halo loader ==========================
-      // Per 8-line batch h: left halo (column k0-1, new values of task c-1),
-      // right halo (column k0+32, old) and, once per plane, the row above the
-      // block (new values of task b-1).  Two batches in flight: the loads of
-      // batch h+1 are issued before batch h's values are stored, so one L2
-      // latency is overlapped with the next poll.
-      const int* lprog = c > 0 ? a.progress + 4 * ((c - 1) * a.Bn + b) : nullptr;
-      const int* uprog = (D == 3 && b > 0) ? a.progress + 4 * (c * a.Bn + (b - 1)) : nullptr;
-      int seenL = 0, seenU = 0;
-      auto up_line = [&](int h) -> int {  // up-halo pseudo-line loaded with batch h, or -1
-        if (D != 3) return -1;
-        if (h == 0) return 0;
-        const int L = 8 * h + 8;
-        return (L % PL == 0 && L < nLines) ? L : -1;
-      };
-      // may batch h be issued?  poll: refresh the neighbours' progress (L2 round trip)
-      auto ready = [&](int h, bool poll) -> bool {
-        const int Lu = up_line(h);
-        const int old = max(Lu, 8 * h + 7) - RU;  // ring predecessors must be dead
-        const int cs = ld_flag(&S.cons);
-        if (cs < old + DEADLAG) return false;
-        if (old >= 0 && ld_flag(&S.wdone) < min(old + 1, nLines)) return false;
-        const int needL = min(8 * h + 8, nLines), needU = Lu >= 0 ? Lu + PL : 0;
-        if (lprog && seenL < needL && poll) {
-          seenL = ld_relaxed(lprog);
+      if (!a.halo_multi) {
+        // ============================ halo loader ==========================
+        // Per 8-line batch h: left halo (column k0-1, new values of task c-1),
+        // right halo (column k0+32, old) and, once per plane, the row above the
+        // block (new values of task b-1).  Two batches in flight: the loads of
+        // batch h+1 are issued before batch h's values are stored, so one L2
+        // latency is overlapped with the next poll.
+        const int* lprog = c > 0 ? a.progress + 4 * ((c - 1) * a.Bn + b) : nullptr;
+        const int* uprog = (D == 3 && b > 0) ? a.progress + 4 * (c * a.Bn + (b - 1)) : nullptr;
+        int seenL = 0, seenU = 0;
+        auto up_line = [&](int h) -> int {  // up-halo pseudo-line loaded with batch h, or -1
+          if (D != 3) return -1;
+          if (h == 0) return 0;
+          const int L = 8 * h + 8;
+          return (L % PL == 0 && L < nLines) ? L : -1;
+        };
+        // may batch h be issued?  poll: refresh the neighbours' progress (L2 round trip)
+        auto ready = [&](int h, bool poll) -> bool {
+          const int Lu = up_line(h);
+          const int old = max(Lu, 8 * h + 7) - RU;  // ring predecessors must be dead
+          const int cs = ld_flag(&S.cons);
+          if (cs < old + DEADLAG) return false;
+          if (old >= 0 && ld_flag(&S.wdone) < min(old + 1, nLines)) return false;
+          const int needL = min(8 * h + 8, nLines), needU = Lu >= 0 ? Lu + PL : 0;
+          if (lprog && seenL < needL && poll) {
+            seenL = ld_relaxed(lprog);
+            if (tr && lane == 0 && seenL >= 8 * 65 && !tr[12]) tr[12] = gtimer();
+          }
+          if (lprog && seenL < needL) return false;
+          if (uprog && seenU < needU && poll) seenU = ld_relaxed(uprog);
+          return !(uprog && seenU < needU);
+        };
+        auto issue = [&](int h, double& hv, double& uw) {
+          if (tr && lane == 0 && h == 64) tr[14] = gtimer();
+          hv = uw = 0.0;
+          if (lane < 16) {  // lanes 0-7: left halo (new), 8-15: right halo (old) of line 8h + (lane & 7)
+            const int L = 8 * h + (lane & 7);
+            int64_t trow;
+            if (ln.kind(L, trow) == 1) hv = __ldcg(a.u + trow * g.P + col0 + (lane < 8 ? -1 : 32));
+          }
+          const int Lu = up_line(h);
+          if (Lu >= 0) {
+            int64_t trow;
+            ln.kind(Lu, trow);
+            uw = __ldcg(a.u + trow * g.P + col0 + lane);
+          }
+        };
+        auto store = [&](int h, double hv, double uw) {
+          if (tr && lane == 0 && h == 64) tr[9] = gtimer();
+          if (lane < 8) {
+            S.u[umod(8 * h + lane - 1, RU)][1] = hv;  // ci = 0 of line 8h + lane
+          } else if (lane < 16) {
+            S.u[umod(8 * h + lane - 8 + 32, RU)][34] = hv;  // ci = 33 of line 8h + lane - 8
+          }
+          const int Lu = up_line(h);
+          if (Lu >= 0) S.u[umod(Lu + lane, RU)][lane + 2] = uw;
+          __syncwarp();
+          if (lane == 0) st_flag(&S.hready, h + 1);
+          if (tr && lane == 0 && h == 64) tr[15] = gtimer();
+        };
+        int hs = 0, hi = 0;  // next batch to store / to issue
+        double hvA = 0.0, uwA = 0.0, hvB = 0.0, uwB = 0.0;
+        while (hs < NHq) {
+          if (hi == hs) {  // slot A empty: block until batch hs may be issued
+            while (!ready(hs, true)) __nanosleep(a.sleep_ns[2]);
+            issue(hs, hvA, uwA);
+            ++hi;
+          }
+          // the progress poll for batch hs+1 is in flight while batch hs is stored
+          // (its result is consumed afterwards; the shared-memory flags carry no
+          // fence, so nothing waits for the outstanding load)
+          const bool want = hi == hs + 1 && hi < NHq;
+          int pL = seenL, pU = seenU;
+          if (want) {
+            if (lprog && seenL < min(8 * hi + 8, nLines)) pL = ld_relaxed(lprog);
+            const int Lu = up_line(hi);
+            if (uprog && Lu >= 0 && seenU < Lu + PL) pU = ld_relaxed(uprog);
+          }
+          store(hs, hvA, uwA);
+          seenL = max(seenL, pL);
+          seenU = max(seenU, pU);
+          if (want && ready(hi, false)) {
+            issue(hi, hvB, uwB);
+            ++hi;
+          }
+          ++hs;
+          hvA = hvB;
+          uwA = uwB;
+        }
+      } else {
+        // ============================ halo loader ==========================
+        // Per 8-line batch h: left halo (column k0-1, new values of task c-1),
+        // right halo (column k0+32, old) and, once per plane, the row above the
+        // block (new values of task b-1).  Each iteration issues one progress
+        // poll (its result is consumed at the end of the iteration) and, in the
+        // same L2 round trip, the loads of every batch already known to be
+        // ready -- up to four batches, one line per lane -- so the loader keeps
+        // pace with the compute warp however far the neighbours' publications
+        // are behind, instead of paying one round trip per batch.
+        const int* lprog = c > 0 ? a.progress + 4 * ((c - 1) * a.Bn + b) : nullptr;
+        const int* uprog = (D == 3 && b > 0) ? a.progress + 4 * (c * a.Bn + (b - 1)) : nullptr;
+        int seenL = lprog ? 0 : (1 << 30), seenU = uprog ? 0 : (1 << 30);
+        auto up_line = [&](int h) -> int {  // up-halo pseudo-line loaded with batch h, or -1
+          if (D != 3) return -1;
+          if (h == 0) return 0;
+          const int L = 8 * h + 8;
+          return (L % PL == 0 && L < nLines) ? L : -1;
+        };
+        // ring cells of batch h dead, neighbours' lines published?
+        auto ready = [&](int h, int cs, int wd) -> bool {
+          const int Lu = up_line(h);
+          const int old = max(Lu, 8 * h + 7) - RU;  // ring predecessors must be dead
+          if (cs < old + DEADLAG) return false;
+          if (old >= 0 && wd < min(old + 1, nLines)) return false;
+          if (seenL < min(8 * h + 8, nLines)) return false;
+          return !(Lu >= 0 && seenU < Lu + PL);
+        };
+        // In flight: loads of batches [hs, hi) (registers), stored next iteration
+        // while the following progress poll is outstanding.
+        int hs = 0, hi = 0;
+        double hv = 0.0, rv = 0.0;
+        bool hl = false;
+        int Lup[3] = {-1, -1, -1};
+        double uw[3] = {0.0, 0.0, 0.0};
+        while (hs < NHq) {
+          // 1. poll the neighbours (consumed after the pending batches are stored)
+          // (only while the neighbours' known progress limits the next batches)
+          int pL = seenL, pU = seenU;
+          const int hn = min(hi + 2, NHq);
+          if (seenL < min(8 * hn, nLines)) pL = ld_relaxed(lprog);
+          if (seenU < min(8 * hn + PL, nLines)) pU = ld_relaxed(uprog);
+          // 2. store the batches loaded last iteration
+          if (hi > hs) {
+            const int L = 8 * hs + lane;
+            if (L < 8 * hi) {
+              S.u[umod(L - 1, RU)][1] = hl ? hv : 0.0;    // ci = 0 of line L
+              S.u[umod(L + 32, RU)][34] = hl ? rv : 0.0;  // ci = 33 of line L
+            }
+  #pragma unroll
+            for (int q = 0; q < 3; ++q)
+              if (Lup[q] >= 0) S.u[umod(Lup[q] + lane, RU)][lane + 2] = uw[q];
+            __syncwarp();
+            if (lane == 0) st_flag(&S.hready, hi);
+            if (tr && lane == 0 && hs <= 64 && 64 < hi) tr[15] = gtimer();
+            hs = hi;
+          }
+          // 3. consume the poll, then issue the loads of every ready batch (<= 4)
+          seenL = max(seenL, pL);
+          seenU = max(seenU, pU);
           if (tr && lane == 0 && seenL >= 8 * 65 && !tr[12]) tr[12] = gtimer();
+          const int cs = ld_flag(&S.cons), wd = ld_flag(&S.wdone);
+          int he = hs;
+          while (he < NHq && he < hs + 4 && ready(he, cs, wd)) ++he;
+          if (he > hs) {
+            if (tr && lane == 0 && hs <= 64 && 64 < he) tr[14] = gtimer();
+            const int L = 8 * hs + lane;  // lane l: left / right halo of line 8 hs + l
+            hv = rv = 0.0;
+            hl = false;
+            if (L < 8 * he) {
+              int64_t trow;
+              if (ln.kind(L, trow) == 1) {
+                const double* row = a.u + trow * g.P + col0;
+                hv = __ldcg(row - 1);
+                rv = __ldcg(row + 32);
+                hl = true;
+              }
+            }
+            // up lines of batches [hs, he): at most three (batch 0 and odd batches)
+            int nu = 0;
+            Lup[0] = Lup[1] = Lup[2] = -1;
+            for (int h = hs; h < he; ++h) {
+              const int Lu = up_line(h);
+              if (Lu >= 0) {
+                if (nu == 0) Lup[0] = Lu;
+                else if (nu == 1) Lup[1] = Lu;
+                else Lup[2] = Lu;
+                ++nu;
+              }
+            }
+  #pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              if (Lup[q] >= 0) {
+                int64_t trow;
+                ln.kind(Lup[q], trow);
+                uw[q] = __ldcg(a.u + trow * g.P + col0 + lane);
+              }
+            }
+            hi = he;
+          } else if (a.sleep_ns[2] > 0) {
+            __nanosleep(a.sleep_ns[2]);
+          }
         }
-        if (lprog && seenL < needL) return false;
-        if (uprog && seenU < needU && poll) seenU = ld_relaxed(uprog);
-        return !(uprog && seenU < needU);
-      };
-      auto issue = [&](int h, double& hv, double& uw) {
-        if (tr && lane == 0 && h == 64) tr[14] = gtimer();
-        hv = uw = 0.0;
-        if (lane < 16) {  // lanes 0-7: left halo (new), 8-15: right halo (old) of line 8h + (lane & 7)
-          const int L = 8 * h + (lane & 7);
-          int64_t trow;
-          if (ln.kind(L, trow) == 1) hv = __ldcg(a.u + trow * g.P + col0 + (lane < 8 ? -1 : 32));
-        }
-        const int Lu = up_line(h);
-        if (Lu >= 0) {
-          int64_t trow;
-          ln.kind(Lu, trow);
-          uw = __ldcg(a.u + trow * g.P + col0 + lane);
-        }
-      };
-      auto store = [&](int h, double hv, double uw) {
-        if (tr && lane == 0 && h == 64) tr[9] = gtimer();
-        if (lane < 8) {
-          S.u[umod(8 * h + lane - 1, RU)][1] = hv;  // ci = 0 of line 8h + lane
-        } else if (lane < 16) {
-          S.u[umod(8 * h + lane - 8 + 32, RU)][34] = hv;  // ci = 33 of line 8h + lane - 8
-        }
-        const int Lu = up_line(h);
-        if (Lu >= 0) S.u[umod(Lu + lane, RU)][lane + 2] = uw;
-        __syncwarp();
-        if (lane == 0) st_flag(&S.hready, h + 1);
-        if (tr && lane == 0 && h == 64) tr[15] = gtimer();
-      };
-      int hs = 0, hi = 0;  // next batch to store / to issue
-      double hvA = 0.0, uwA = 0.0, hvB = 0.0, uwB = 0.0;
-      while (hs < NHq) {
-        if (hi == hs) {  // slot A empty: block until batch hs may be issued
-          while (!ready(hs, true)) __nanosleep(a.sleep_ns[2]);
-          issue(hs, hvA, uwA);
-          ++hi;
-        }
-        // the progress poll for batch hs+1 is in flight while batch hs is stored
-        // (its result is consumed afterwards; the shared-memory flags carry no
-        // fence, so nothing waits for the outstanding load)
-        const bool want = hi == hs + 1 && hi < NHq;
-        int pL = seenL, pU = seenU;
-        if (want) {
-          if (lprog && seenL < min(8 * hi + 8, nLines)) pL = ld_relaxed(lprog);
-          const int Lu = up_line(hi);
-          if (uprog && Lu >= 0 && seenU < Lu + PL) pU = ld_relaxed(uprog);
-        }
-        store(hs, hvA, uwA);
-        seenL = max(seenL, pL);
-        seenU = max(seenU, pU);
-        if (want && ready(hi, false)) {
-          issue(hi, hvB, uwB);
-          ++hi;
-        }
-        ++hs;
-        hvA = hvB;
-        uwA = uwB;
       }
     } else if (warp == 3) {
       // ============================ writer ===============================
