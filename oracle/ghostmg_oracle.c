@@ -187,6 +187,46 @@ void oracle_extrapolate(int d, int64_t N, int ngroups, const int64_t *group_len,
   }
 }
 
+/* The two phases of oracle_extrapolate on a subset of the band, for the
+ * z-slab schedule tests (tests/test_slabs.py): one BFS group over the nodes
+ * idx[0..m) (same arithmetic as above), and one Jacobi transport step over
+ * them (all reads before any write, like the reference's vectorised step). */
+void oracle_band_bfs(int d, int64_t N, int64_t m, const int64_t *idx, const uint8_t *mask, double *out) {
+  int64_t n = N + 1, s[3];
+  strides64(d, n, s);
+  double t[6];
+  for (int64_t q = 0; q < m; ++q) {
+    int64_t i = idx[q];
+    uint8_t mk = mask[q];
+    int cnt = 0;
+    for (int k = 0; k < d; ++k)
+      for (int j = 0; j < 2; ++j) {
+        int bit = (mk >> (2 * k + j)) & 1;
+        int64_t nbr = bit ? (j ? i + s[k] : i - s[k]) : i;
+        t[2 * k + j] = out[nbr] * (bit ? 1.0 : 0.0);
+        cnt += bit;
+      }
+    out[i] = seq_sum(t, 2 * d) / (double)cnt;
+  }
+}
+
+void oracle_band_transport(int d, int64_t N, int64_t m, const int64_t *idx, const int8_t *step,
+                           const double *absn, double *out, double *scratch) {
+  int64_t n = N + 1, s[3];
+  strides64(d, n, s);
+  double t[3];
+  for (int64_t q = 0; q < m; ++q) {
+    int64_t i = idx[q];
+    double vi = out[i];
+    for (int k = 0; k < d; ++k) {
+      int64_t nbr = i - (int64_t)step[q * d + k] * s[k];
+      t[k] = absn[q * d + k] * (vi - out[nbr]);
+    }
+    scratch[q] = vi - 0.5 * seq_sum(t, d);
+  }
+  for (int64_t q = 0; q < m; ++q) out[idx[q]] = scratch[q];
+}
+
 /* ---- restrictions ------------------------------------------------------
  * InteriorRestriction.apply (transfer.py:64-93): per coarse internal node,
  * pairwise(w * r[3^d fine block around 2m]) with w = full weighting, or

@@ -36,6 +36,8 @@ def lib():
             "oracle_residual_internal": (_d, [ctypes.c_int, _i64, _p, _p, _p, _d, _d, _p]),
             "oracle_residual_ghost": (_d, [ctypes.c_int, _i64, _p, _p, _p, _p, _p]),
             "oracle_extrapolate": (None, [ctypes.c_int, _i64, ctypes.c_int, _p, _p, _p, _p, _p, _p, _p]),
+            "oracle_band_bfs": (None, [ctypes.c_int, _i64, _i64, _p, _p, _p]),
+            "oracle_band_transport": (None, [ctypes.c_int, _i64, _i64, _p, _p, _p, _p, _p]),
             "oracle_restrict_interior": (None, [ctypes.c_int, _i64, _p, _p, _p, _p]),
             "oracle_restrict_ghost": (None, [ctypes.c_int, _i64, _p, _p, _i64, _p, _p]),
             "oracle_interpolate_add": (None, [ctypes.c_int, _i64, _p, _p, _p]),
@@ -108,6 +110,22 @@ def extrapolate(plan, values):
                              _ptr(plan.band_idx), _ptr(_c(plan.bfs_mask, np.uint8)), _ptr(step),
                              _ptr(absn), _ptr(values), _ptr(scratch))
     return values
+
+
+def band_bfs(plan, values, idx, mask):
+    """One BFS group of the band extension on the nodes ``idx`` (in place)."""
+    idx = _c(idx, np.int64)
+    if idx.size:
+        lib().oracle_band_bfs(plan.d, plan.N, idx.size, _ptr(idx), _ptr(_c(mask, np.uint8)), _ptr(values))
+
+
+def band_transport(plan, values, idx, step, absn):
+    """One Jacobi transport step of the band extension on the nodes ``idx``."""
+    idx = _c(idx, np.int64)
+    if idx.size:
+        scratch = np.empty(idx.size)
+        lib().oracle_band_transport(plan.d, plan.N, idx.size, _ptr(idx), _ptr(_c(step, np.int8)),
+                                    _ptr(_c(absn, np.float64)), _ptr(values), _ptr(scratch))
 
 
 def restrict_interior(fine, coarse, r_fine):
