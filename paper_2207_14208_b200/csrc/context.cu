@@ -471,7 +471,8 @@ int op_smooth(gmg_ctx* ctx, DevLevel& l, int count) {
 
 int op_res_int(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
   Scope s(ctx, slot ? 7 : 2);
-  launch_residual_interior(l.g, l.labels, l.u, l.f, l.rI, slot, ctx->stream);
+  // the norm pass (slot set) only needs the maximum: no residual array writes
+  launch_residual_interior(l.g, l.labels, l.u, l.f, slot ? nullptr : l.rI, slot, ctx->stream);
   ctx->launches++;
   return 0;
 }
@@ -479,7 +480,7 @@ int op_res_int(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
 int op_res_ghost(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
   if (l.ng == 0) return 0;
   Scope s(ctx, slot ? 7 : 2);
-  launch_residual_ghost(ghost_args(l), l.u, l.rE, slot, ctx->stream);
+  launch_residual_ghost(ghost_args(l), l.u, slot ? nullptr : l.rE, slot, ctx->stream);
   ctx->launches++;
   return 0;
 }

@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(256) residual_ghost_kernel(GhostArgs a, const 
 #pragma unroll
     for (int j = 0; j < M; ++j) p[j] = __ldg(a.w + (int64_t)j * a.ng + s) * u[base + block_offset<D>(a.g, j)];
     const double r = a.gval[s] - np_sum<M>(p);
-    r_ext[a.node[s]] = r;
+    if (r_ext) r_ext[a.node[s]] = r;
     am = fabs(r);
   }
   block_max_commit(am, maxbits);

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) residual_interior_kernel(Geom g, const ui
       s = ((u[i - g.s0] + u[i + g.s0]) + u[i - 1]) + u[i + 1];
     s = s + 0.0;
     const double v = (f[i] - g.c * u[i]) + div_h2(g, s);
-    r[i] = v;
+    if (r) r[i] = v;
     am = (__double_as_longlong(fabs(v)) > __double_as_longlong(am)) ? fabs(v) : am;
   }
   block_max_commit(am, maxbits);
