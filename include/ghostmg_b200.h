@@ -97,6 +97,17 @@ int gmg_set_coarse_callback(gmg_ctx *ctx, gmg_coarse_cb cb, void *user);
  * coarsest level, ordered like gmg_coarse_cb's rhs) for coarse_mode 2; the
  * pointer is host memory or (on_device != 0) device memory, copied. */
 int gmg_set_coarse_inverse(gmg_ctx *ctx, int64_t n, const double *inv, int on_device);
+/* The same coarse_mode-2 solve by one level of nested dissection (takes
+ * precedence over the dense inverse): the n unknowns permuted to [A | B | S]
+ * (perm[i] = index in gmg_coarse_cb's rhs order of permuted unknown i; A and B
+ * decoupled, S their separator), row-major blocks AAi (na x na) = A_AA^-1,
+ * BBi (nb x nb) = A_BB^-1, G (ns x (na+nb)) = [A_SA AAi, A_SB BBi],
+ * W ((na+nb) x ns) = [AAi A_AS; BBi A_BS], Si (ns x ns) = the inverse Schur
+ * complement.  Host or (on_device != 0) device pointers, copied.
+ * Replaces the reference's splu solve (solver.py:146-166) like the inverse. */
+int gmg_set_coarse_nd(gmg_ctx *ctx, int64_t n, int64_t na, int64_t nb, int64_t ns, const int32_t *perm,
+                      const double *aai, const double *bbi, const double *g, const double *w,
+                      const double *si, int on_device);
 
 /* Host <-> device copies of a level vector (see enum gmg_vector). */
 int gmg_set_vector(gmg_ctx *ctx, int level, int which, const double *host);

@@ -40,6 +40,7 @@ SIGNATURES = {
     "gmg_set_cycle": (_i, [_p, _i, _i, _i, _i, _i, _i]),
     "gmg_set_coarse_callback": (_i, [_p, COARSE_CB, _p]),
     "gmg_set_coarse_inverse": (_i, [_p, _i64, _p, _i]),
+    "gmg_set_coarse_nd": (_i, [_p, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _i]),
     "gmg_set_vector": (_i, [_p, _i, _i, _p]),
     "gmg_get_vector": (_i, [_p, _i, _i, _p]),
     "gmg_device_pointer": (_p, [_p, _i, _i]),
@@ -163,6 +164,12 @@ class Context:
 
     def set_coarse_inverse(self, n, ptr_value, on_device):
         self.check(self.lib.gmg_set_coarse_inverse(self.ctx, n, ptr_value, 1 if on_device else 0))
+
+    def set_coarse_nd(self, n, na, nb, ns, perm, aai, bbi, g, w, si, on_device):
+        """Nested-dissection coarse solve (pointers: device if on_device)."""
+        perm = np.ascontiguousarray(perm, dtype=np.int32)
+        self.check(self.lib.gmg_set_coarse_nd(self.ctx, n, na, nb, ns, ptr(perm), aai, bbi, g, w, si,
+                                              1 if on_device else 0))
 
     def set_stream(self, stream_handle):
         self.check(self.lib.gmg_set_stream(self.ctx, stream_handle))

@@ -74,6 +74,14 @@ struct DevLevel {
   double *rhs_d = nullptr, *x_d = nullptr, *rhs_h = nullptr, *x_h = nullptr;
   double *cinv = nullptr, *cpart = nullptr;  // device dense inverse of the coarsest operator
   int64_t cinv_n = 0;
+  // nested-dissection form of the same solve: unknowns permuted to [A | B | S]
+  // (two plane halves and their separator); inverses of the A and B blocks,
+  // G = [A_SA AAi, A_SB BBi], W = [AAi A_AS; BBi A_BS], Si = Schur complement^-1
+  int64_t nd_n = 0, nd_a = 0, nd_b = 0, nd_s = 0;
+  int32_t* nd_perm = nullptr;   // permuted position -> active index
+  int64_t* nd_pos = nullptr;    // permuted position -> grid position
+  double *nd_aai = nullptr, *nd_bbi = nullptr, *nd_g = nullptr, *nd_w = nullptr, *nd_si = nullptr;
+  double *nd_b_ = nullptr, *nd_x = nullptr, *nd_t = nullptr, *nd_part = nullptr;
   bool ready = false;
 };
 
@@ -175,7 +183,8 @@ void free_level(DevLevel& l) {
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
                   l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
                   l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off,
-                  l.bfixpos, l.bnbr, l.bv0, l.bv1};  // ticket lives in progress
+                  l.bfixpos, l.bnbr, l.bv0, l.bv1, l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g,
+                  l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -535,6 +544,21 @@ int coarse_solve(gmg_ctx* ctx, int li) {
   GMG_CHECK(ctx, cudaMemsetAsync(l.u, 0, sizeof(double) * (size_t)l.g.nodes, ctx->stream));
   if (ctx->coarse_mode == 1) return op_smooth(ctx, l, ctx->coarse_sweeps);
   const int64_t n = l.n_int + l.ng;
+  if (ctx->coarse_mode == 2 && l.nd_n == n) {
+    // x = A^-1 rhs by one level of nested dissection (5 GEMVs, ~60 % of the
+    // dense inverse's bytes)
+    const int64_t na = l.nd_a, nb = l.nd_b, ns = l.nd_s, nab = na + nb;
+    launch_gather(l.active, l.n_int, l.f, l.lex2slot, l.ng, l.gval, l.rhs_d, ctx->stream);
+    launch_permute(l.rhs_d, l.nd_perm, n, l.nd_b_, ctx->stream);
+    launch_gemv_rect(l.nd_aai, l.nd_b_, na, na, l.nd_part, nullptr, l.nd_x, ctx->stream);
+    launch_gemv_rect(l.nd_bbi, l.nd_b_ + na, nb, nb, l.nd_part, nullptr, l.nd_x + na, ctx->stream);
+    launch_gemv_rect(l.nd_g, l.nd_b_, ns, nab, l.nd_part, l.nd_b_ + nab, l.nd_t, ctx->stream);
+    launch_gemv_rect(l.nd_si, l.nd_t, ns, ns, l.nd_part, nullptr, l.nd_x + nab, ctx->stream);
+    launch_gemv_rect(l.nd_w, l.nd_x + nab, nab, ns, l.nd_part, l.nd_x, l.nd_x, ctx->stream);
+    launch_scatter(l.nd_pos, n, l.nd_x, l.u, ctx->stream);
+    ctx->launches += 13;
+    return 0;
+  }
   if (ctx->coarse_mode == 2) {
     if (!l.cinv || l.cinv_n != n) return fail(ctx, "device coarse mode needs gmg_set_coarse_inverse");
     launch_gather(l.active, l.n_int, l.f, l.lex2slot, l.ng, l.gval, l.rhs_d, ctx->stream);
@@ -1000,6 +1024,50 @@ int gmg_set_coarse_inverse(gmg_ctx* ctx, int64_t n, const double* inv, int on_de
   GMG_CHECK(ctx, cudaMemcpy(l.cinv, inv, sizeof(double) * (size_t)(n * n),
                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
   l.cinv_n = n;
+  return 0;
+}
+
+int gmg_set_coarse_nd(gmg_ctx* ctx, int64_t n, int64_t na, int64_t nb, int64_t ns, const int32_t* perm,
+                      const double* aai, const double* bbi, const double* g, const double* w, const double* si,
+                      int on_device) {
+  DevLevel& l = ctx->L[ctx->nlevels - 1];
+  if (!l.ready) return fail(ctx, "coarsest level not set");
+  if (n != l.n_int + l.ng || na + nb + ns != n || na <= 0 || nb <= 0 || ns <= 0)
+    return fail(ctx, "nested-dissection sizes do not match the coarsest level");
+  cudaSetDevice(ctx->device);
+  graph_reset(ctx);
+  void* old[] = {l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g, l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part};
+  for (void* p : old)
+    if (p) cudaFree(p);
+  l.nd_perm = nullptr;
+  l.nd_pos = nullptr;
+  l.nd_aai = l.nd_bbi = l.nd_g = l.nd_w = l.nd_si = l.nd_b_ = l.nd_x = l.nd_t = l.nd_part = nullptr;
+  l.nd_n = 0;
+  const int64_t nab = na + nb;
+  int64_t part = std::max({gemv_rect_part_size(na, na), gemv_rect_part_size(nb, nb), gemv_rect_part_size(ns, nab),
+                           gemv_rect_part_size(ns, ns), gemv_rect_part_size(nab, ns)});
+  // the active-order index and grid position of every permuted unknown
+  std::vector<int64_t> act((size_t)n), pos((size_t)n);
+  GMG_CHECK(ctx, cudaMemcpy(act.data(), l.active, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < n; ++i) {
+    if (perm[i] < 0 || perm[i] >= n) return fail(ctx, "nested-dissection permutation out of range");
+    pos[i] = act[perm[i]];
+  }
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (upload(ctx, &l.nd_perm, perm, n) || upload(ctx, &l.nd_pos, pos.data(), n) || dalloc(ctx, &l.nd_aai, na * na) ||
+      dalloc(ctx, &l.nd_bbi, nb * nb) || dalloc(ctx, &l.nd_g, ns * nab) || dalloc(ctx, &l.nd_w, nab * ns) ||
+      dalloc(ctx, &l.nd_si, ns * ns) || dalloc(ctx, &l.nd_b_, n) || dalloc(ctx, &l.nd_x, n) ||
+      dalloc(ctx, &l.nd_t, ns) || dalloc(ctx, &l.nd_part, part))
+    return -1;
+  GMG_CHECK(ctx, cudaMemcpy(l.nd_aai, aai, sizeof(double) * (size_t)(na * na), kind));
+  GMG_CHECK(ctx, cudaMemcpy(l.nd_bbi, bbi, sizeof(double) * (size_t)(nb * nb), kind));
+  GMG_CHECK(ctx, cudaMemcpy(l.nd_g, g, sizeof(double) * (size_t)(ns * nab), kind));
+  GMG_CHECK(ctx, cudaMemcpy(l.nd_w, w, sizeof(double) * (size_t)(nab * ns), kind));
+  GMG_CHECK(ctx, cudaMemcpy(l.nd_si, si, sizeof(double) * (size_t)(ns * ns), kind));
+  l.nd_n = n;
+  l.nd_a = na;
+  l.nd_b = nb;
+  l.nd_s = ns;
   return 0;
 }
 

@@ -99,6 +99,9 @@ void launch_gather(const int64_t* idx, int64_t n_int, const double* f, const int
 void launch_scatter(const int64_t* idx, int64_t n, const double* x, double* e, cudaStream_t st);
 void launch_dense_gemv(const double* A, const double* x, int64_t n, double* part, double* y, cudaStream_t st);
 int gemv_chunks(int64_t n);
+void launch_gemv_rect(const double* A, const double* x, int64_t m, int64_t k, double* part, const double* y0,
+                      double* y, cudaStream_t st);
+int64_t gemv_rect_part_size(int64_t m, int64_t k);
 void launch_repitch(const double* src, double* dst, int64_t rows, int64_t n, int64_t P, bool to_padded,
                     cudaStream_t st);
 void launch_permute(const double* src, const int32_t* perm, int64_t n, double* dst,

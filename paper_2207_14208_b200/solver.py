@@ -69,13 +69,19 @@ class DeviceHierarchy:
         elif coarse_mode == 2:
             self._upload_inverse()
 
+    ND_MIN = 8192  # coarsest systems at least this large use the nested-dissection form
+
     def _upload_inverse(self):
         """Invert the coarsest operator on the GPU (setup) and hand it to the
-        library, which copies it into its own buffer."""
+        library, which copies it into its own buffer: for large systems as one
+        level of nested dissection (two decoupled plane halves + separator),
+        else as one dense inverse."""
         import torch
 
-        A, _ = coarsest_system(self.plans[-1])
+        A, active = coarsest_system(self.plans[-1])
         n = A.shape[0]
+        if n >= self.ND_MIN and self._upload_nd(A, active):
+            return
         dev = torch.device("cuda", self.device_index)
         dense = torch.from_numpy(A.toarray()).to(dev)
         inv = torch.linalg.inv(dense).contiguous()  # LAPACK-backed results may be column-major
@@ -84,6 +90,58 @@ class DeviceHierarchy:
         self.ctx.set_coarse_inverse(n, inv.data_ptr(), True)
         del inv
         torch.cuda.empty_cache()
+
+    def _nd_split(self, A, active):
+        """[A | B | S] split of the coarsest unknowns by axis-0 planes: the
+        narrowest separator around the middle plane that decouples the halves
+        (the 3^d ghost rows reach two planes), or None."""
+        p = self.plans[-1]
+        per = (p.N + 1) ** (p.d - 1)
+        planes = np.asarray(active) // per
+        mid = p.N // 2
+        csr = A.tocsr()
+        for w in range(1, max(2, p.N // 4)):
+            a = np.flatnonzero(planes < mid - w)
+            b = np.flatnonzero(planes > mid + w)
+            sep = np.flatnonzero((planes >= mid - w) & (planes <= mid + w))
+            if len(a) == 0 or len(b) == 0:
+                return None
+            if csr[a][:, b].nnz == 0 and csr[b][:, a].nnz == 0:
+                return a, b, sep
+        return None
+
+    def _upload_nd(self, A, active):
+        import torch
+
+        split = self._nd_split(A, active)
+        if split is None:
+            return False
+        a, b, sep = split
+        dev = torch.device("cuda", self.device_index)
+        csr = A.tocsr()
+
+        def blk(r, c):
+            return torch.from_numpy(csr[r][:, c].toarray()).to(dev)
+
+        aai = torch.linalg.inv(blk(a, a))
+        bbi = torch.linalg.inv(blk(b, b))
+        asp, bsp = blk(a, sep), blk(b, sep)
+        sa, sb = blk(sep, a), blk(sep, b)
+        wa, wb = aai @ asp, bbi @ bsp
+        ga, gb = sa @ aai, sb @ bbi
+        schur = blk(sep, sep) - sa @ wa - sb @ wb
+        si = torch.linalg.inv(schur).contiguous()
+        g = torch.cat([ga, gb], dim=1).contiguous()
+        w = torch.cat([wa, wb], dim=0).contiguous()
+        aai, bbi = aai.contiguous(), bbi.contiguous()
+        torch.cuda.synchronize(dev)
+        perm = np.concatenate([a, b, sep]).astype(np.int32)
+        self.ctx.set_coarse_nd(len(perm), len(a), len(b), len(sep), perm, aai.data_ptr(), bbi.data_ptr(),
+                               g.data_ptr(), w.data_ptr(), si.data_ptr(), True)
+        self.nd_sizes = (len(a), len(b), len(sep))
+        del aai, bbi, g, w, si, asp, bsp, sa, sb, wa, wb, ga, gb, schur
+        torch.cuda.empty_cache()
+        return True
 
     def _factor(self):
         if self._lu is None:

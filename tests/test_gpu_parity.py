@@ -163,3 +163,28 @@ def test_device_inverse_coarse_solve_within_tolerance(gpu_available):
     uref, _ = ref.solve(u=np.zeros(plans[0].n_nodes), cycles=rec["cycles"])
     assert np.max(np.abs(u - uref)) <= 1e-12 * np.max(np.abs(uref))
     assert abs(measure_rho(solver, seed=42).rho_asymptotic - rec["rho"]["rho"]) < 1e-3
+
+
+def test_nested_dissection_coarse_solve_within_tolerance(gpu_available):
+    """coarse_backend='device-inverse' on a coarsest level large enough for
+    the nested-dissection form (pores 64^3 down to N=32: ~28k unknowns):
+    same tolerances as the dense inverse against the bitwise SuperLU path."""
+    from paper_2207_14208_b200 import configs as CF
+    from paper_2207_14208_b200.cycle import CycleDriver
+    from paper_2207_14208_b200.transfer import build_hierarchy
+
+    setup = CF.config_pores(N=64, cycles=12, coarsest_min=32)
+    levels = build_hierarchy(setup.grid, setup.phi, setup.faces, coarsest_min=setup.coarsest_min)
+    plans, f, g, e = CycleDriver.problem_data(levels, setup.spec, setup.smoother, setup.default_variant)
+    f = CF.pore_rhs(setup, plans[0].labels)
+    nd = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, coarse_backend="device-inverse")
+    assert getattr(nd.device, "nd_sizes", None), "nested dissection not used"
+    ref = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, coarse_backend="superlu")
+    u, rep = nd.solve(u=np.zeros(plans[0].n_nodes), cycles=12)
+    uref, rref = ref.solve(u=np.zeros(plans[0].n_nodes), cycles=12)
+    want = np.array(rref.residual_norms)
+    got = np.array(rep.residual_norms)
+    early = want > 1e-4 * want[0]
+    assert early.sum() >= 6
+    assert np.max(np.abs(got - want)[early] / want[early]) < 1e-10
+    assert np.max(np.abs(u - uref)) <= 1e-12 * np.max(np.abs(uref))
