@@ -603,7 +603,29 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         (void)leadF;
       }
     } else if (warp == 2) {
-      if (!a.halo_multi) {
+      if (a.variant == 7 || a.variant >= 1000) {
+        // DIAGNOSTIC ONLY (wrong results): publish every halo batch as soon as
+        // its ring cells are free, without waiting for the neighbours or
+        // loading anything -- the sweep time without halo costs (variant 7).
+        // Variant 1000 + X first waits until both neighbours have published X
+        // lines: the wavefront's start stagger without its steady-state
+        // coupling (tools/gs_tune.py).
+        if (a.variant >= 1000) {
+          const int X = a.variant - 1000;
+          const int* lp = c > 0 ? a.progress + 4 * ((c - 1) * a.Bn + b) : nullptr;
+          const int* up = (D == 3 && b > 0) ? a.progress + 4 * (c * a.Bn + (b - 1)) : nullptr;
+          while ((lp && ld_relaxed(lp) < min(X, nLines)) || (up && ld_relaxed(up) < min(X, nLines))) __nanosleep(200);
+        }
+        for (int h = 0; h < NHq; ++h) {
+          const int old = 8 * h + 7 - RU;
+          for (;;) {
+            const int cs = ld_flag(&S.cons);
+            if (cs >= old + DEADLAG && (old < 0 || ld_flag(&S.wdone) >= min(old + 1, nLines))) break;
+            __nanosleep(100);
+          }
+          if (lane == 0) st_flag(&S.hready, h + 1);
+        }
+      } else if (!a.halo_multi) {
         // ============================ halo loader ==========================
         // Per 8-line batch h: left halo (column k0-1, new values of task c-1),
         // right halo (column k0+32, old) and, once per plane, the row above the
