@@ -9,6 +9,7 @@
 // correction, nu2 smoothing steps.  Nothing leaves the device except the
 // coarsest right-hand side when the host SuperLU callback is used.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -22,6 +23,20 @@
 using namespace gmg;
 
 namespace {
+
+// NumPy pairwise-sum tree of a compacted vector of length n (see
+// l2_leaf_*_kernel): leaves of <= 128 elements in order, internal nodes
+// combined height by height.
+struct PwTree {
+  int64_t n = -1;
+  int64_t nleaves = 0, nnodes = 0;
+  int32_t root = -1;
+  std::vector<int64_t> level_off;       // internal nodes of height h at [level_off[h], level_off[h+1])
+  int64_t *d_a = nullptr, *d_b = nullptr;  // leaf (start, end) positions or (offset, -) list entries
+  int32_t* d_len = nullptr;
+  int32_t *d_ca = nullptr, *d_cb = nullptr, *d_cd = nullptr;  // children / destination per internal node
+  double* d_vals = nullptr;
+};
 
 struct DevLevel {
   Geom g{};
@@ -82,6 +97,7 @@ struct DevLevel {
   int64_t* nd_pos = nullptr;    // permuted position -> grid position
   double *nd_aai = nullptr, *nd_bbi = nullptr, *nd_g = nullptr, *nd_w = nullptr, *nd_si = nullptr;
   double *nd_b_ = nullptr, *nd_x = nullptr, *nd_t = nullptr, *nd_part = nullptr;
+  PwTree l2i, l2g;  // l2 residual norm: internal nodes (lex order), ghosts (lex order)
   bool ready = false;
 };
 
@@ -178,7 +194,16 @@ int upload(gmg_ctx* ctx, T** p, const T* host, int64_t count) {
   return 0;
 }
 
+void free_tree(PwTree& t) {
+  void* p[] = {t.d_a, t.d_b, t.d_len, t.d_ca, t.d_cb, t.d_cd, t.d_vals};
+  for (void* q : p)
+    if (q) cudaFree(q);
+  t = PwTree();
+}
+
 void free_level(DevLevel& l) {
+  free_tree(l.l2i);
+  free_tree(l.l2g);
   void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
                   l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
@@ -626,6 +651,142 @@ int stage_for(gmg_ctx* ctx, const DevLevel& l) {
   }
   if (dalloc(ctx, &ctx->stage, need)) return -1;
   ctx->stage_n = need;
+  return 0;
+}
+
+// ---- l2 norm: NumPy pairwise tree --------------------
+int64_t pw_count_leaves(int64_t n) {
+  if (n <= 128) return 1;
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return pw_count_leaves(n2) + pw_count_leaves(n - n2);
+}
+
+// returns (node id, height); leaves get ids 0.. in order, internal nodes L..
+std::pair<int32_t, int> pw_build(int64_t off, int64_t n, std::vector<int64_t>& leaf_off, std::vector<int32_t>& leaf_len,
+                                 std::vector<std::vector<std::array<int32_t, 2>>>& by_h,
+                                 std::vector<std::vector<int32_t>>& dst_h, int32_t& next_internal) {
+  if (n <= 128) {
+    leaf_off.push_back(off);
+    leaf_len.push_back((int32_t)n);
+    return {(int32_t)(leaf_off.size() - 1), 0};
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  auto a = pw_build(off, n2, leaf_off, leaf_len, by_h, dst_h, next_internal);
+  auto b = pw_build(off + n2, n - n2, leaf_off, leaf_len, by_h, dst_h, next_internal);
+  const int h = std::max(a.second, b.second) + 1;
+  if ((int)by_h.size() < h) {
+    by_h.resize(h);
+    dst_h.resize(h);
+  }
+  const int32_t id = next_internal++;
+  by_h[h - 1].push_back({a.first, b.first});
+  dst_h[h - 1].push_back(id);
+  return {id, h};
+}
+
+// build tree t for n elements; leaf k covers compact [leaf_off[k], +leaf_len[k]);
+// `ends` maps the leaves to the two int64 values the leaf kernel needs
+template <class EndsFn>
+int pw_setup(gmg_ctx* ctx, PwTree& t, int64_t n, EndsFn ends) {
+  free_tree(t);
+  t.n = n;
+  if (n == 0) return 0;
+  std::vector<int64_t> leaf_off;
+  std::vector<int32_t> leaf_len;
+  std::vector<std::vector<std::array<int32_t, 2>>> by_h;
+  std::vector<std::vector<int32_t>> dst_h;
+  const int64_t L = pw_count_leaves(n);
+  int32_t next = (int32_t)L;
+  auto root = pw_build(0, n, leaf_off, leaf_len, by_h, dst_h, next);
+  t.nleaves = L;
+  t.nnodes = next;
+  t.root = root.first;
+  std::vector<int64_t> a((size_t)L), b((size_t)L);
+  ends(leaf_off, leaf_len, a, b);
+  std::vector<int32_t> ca, cb, cd;
+  t.level_off.assign(1, 0);
+  for (size_t h = 0; h < by_h.size(); ++h) {
+    for (size_t k = 0; k < by_h[h].size(); ++k) {
+      ca.push_back(by_h[h][k][0]);
+      cb.push_back(by_h[h][k][1]);
+      cd.push_back(dst_h[h][k]);
+    }
+    t.level_off.push_back((int64_t)ca.size());
+  }
+  if (upload(ctx, &t.d_a, a.data(), L) || upload(ctx, &t.d_b, b.data(), L) ||
+      upload(ctx, &t.d_len, leaf_len.data(), L) || upload(ctx, &t.d_ca, ca.data(), (int64_t)ca.size()) ||
+      upload(ctx, &t.d_cb, cb.data(), (int64_t)cb.size()) || upload(ctx, &t.d_cd, cd.data(), (int64_t)cd.size()) ||
+      dalloc(ctx, &t.d_vals, t.nnodes))
+    return -1;
+  return 0;
+}
+
+void pw_combine(gmg_ctx* ctx, PwTree& t) {
+  for (size_t h = 0; h + 1 < t.level_off.size(); ++h) {
+    const int64_t o = t.level_off[h], m = t.level_off[h + 1] - o;
+    launch_l2_combine(t.d_vals, t.d_ca + o, t.d_cb + o, t.d_cd + o, m, ctx->stream);
+    ctx->launches++;
+  }
+}
+
+// sum of squares of the internal residuals (lex order) and the ghost
+// residuals (lex order), each 0.0 + pairwise like NumPy's .sum()
+int l2_parts(gmg_ctx* ctx, DevLevel& l, double* out) {
+  if (l.l2i.n < 0) {
+    // leaf boundaries: grid positions of the first / one past the last internal node
+    const int64_t nodes = l.g.nodes;
+    std::vector<uint8_t> lab((size_t)nodes);
+    GMG_CHECK(ctx, cudaMemcpy(lab.data(), l.labels, (size_t)nodes, cudaMemcpyDeviceToHost));
+    int64_t ni = 0;
+    for (int64_t p = 0; p < nodes; ++p) ni += lab[p] == INTERNAL;
+    auto ends = [&](const std::vector<int64_t>& off, const std::vector<int32_t>& len, std::vector<int64_t>& a,
+                    std::vector<int64_t>& b) {
+      size_t k = 0;
+      int64_t c = 0;
+      for (int64_t p = 0; p < nodes && k < off.size(); ++p) {
+        if (lab[p] != INTERNAL) continue;
+        if (c == off[k]) a[k] = p;
+        if (c == off[k] + len[k] - 1) {
+          b[k] = p + 1;
+          ++k;
+        }
+        ++c;
+      }
+    };
+    if (pw_setup(ctx, l.l2i, ni, ends)) return -1;
+    auto list = [&](const std::vector<int64_t>& off, const std::vector<int32_t>&, std::vector<int64_t>& a,
+                    std::vector<int64_t>& b) {
+      for (size_t k = 0; k < off.size(); ++k) a[k] = off[k], b[k] = 0;
+    };
+    if (pw_setup(ctx, l.l2g, l.ng, list)) return -1;
+  }
+  double parts[2] = {0.0, 0.0};
+  if (l.l2i.n > 0) {
+    launch_l2_leaves_scan(l.labels, l.rI, l.l2i.d_a, l.l2i.d_b, l.l2i.d_len, l.l2i.nleaves, l.l2i.d_vals,
+                          ctx->stream);
+    ctx->launches++;
+    pw_combine(ctx, l.l2i);
+  }
+  if (l.l2g.n > 0) {
+    launch_l2_leaves_list(l.rE, l.gnode, l.lex2slot, l.l2g.d_a, l.l2g.d_len, l.l2g.nleaves, l.l2g.d_vals,
+                          ctx->stream);
+    ctx->launches++;
+    pw_combine(ctx, l.l2g);
+  }
+  double v[2] = {0.0, 0.0};
+  if (l.l2i.n > 0)
+    GMG_CHECK(ctx, cudaMemcpyAsync(&v[0], l.l2i.d_vals + l.l2i.root, sizeof(double), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+  if (l.l2g.n > 0)
+    GMG_CHECK(ctx, cudaMemcpyAsync(&v[1], l.l2g.d_vals + l.l2g.root, sizeof(double), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  parts[0] = l.l2i.n > 0 ? 0.0 + v[0] : 0.0;
+  parts[1] = l.l2g.n > 0 ? 0.0 + v[1] : 0.0;
+  out[0] = parts[0];
+  out[1] = parts[1];
   return 0;
 }
 
@@ -1230,10 +1391,17 @@ int gmg_cycle(gmg_ctx* ctx, int ncycles) {
 
 int gmg_residual_norm(gmg_ctx* ctx, int li, double* out) {
   if (li < 0 || li >= ctx->nlevels || !ctx->L[li].ready) return fail(ctx, "level not set");
-  if (ctx->norm != 0) return fail(ctx, "l2 norm is not available on the device path yet");
   cudaSetDevice(ctx->device);
   DevLevel& l = ctx->L[li];
   ctx->cur_level = li;
+  if (ctx->norm == 1) {
+    // l2: the two sums of squares (the caller takes sqrt(a + b), solver.py:138)
+    if (op_res_int(ctx, l, nullptr) || op_res_ghost(ctx, l, nullptr)) return -1;
+    if (l2_parts(ctx, l, out)) return -1;
+    GMG_CHECK(ctx, cudaGetLastError());
+    if (ctx->prof) profile_flush(ctx);
+    return 0;
+  }
   GMG_CHECK(ctx, cudaMemsetAsync(ctx->dmax, 0, 2 * sizeof(unsigned long long), ctx->stream));
   if (op_res_int(ctx, l, ctx->dmax)) return -1;
   if (op_res_ghost(ctx, l, ctx->dmax + 1)) return -1;

@@ -104,6 +104,12 @@ void launch_gemv_rect(const double* A, const double* x, int64_t m, int64_t k, do
 int64_t gemv_rect_part_size(int64_t m, int64_t k);
 void launch_repitch(const double* src, double* dst, int64_t rows, int64_t n, int64_t P, bool to_padded,
                     cudaStream_t st);
+void launch_l2_leaves_scan(const uint8_t* lab, const double* r, const int64_t* start, const int64_t* end,
+                           const int32_t* len, int64_t nleaves, double* vals, cudaStream_t st);
+void launch_l2_leaves_list(const double* x, const int64_t* pos, const int32_t* slot, const int64_t* off,
+                           const int32_t* len, int64_t nleaves, double* vals, cudaStream_t st);
+void launch_l2_combine(double* vals, const int32_t* a, const int32_t* b, const int32_t* dst, int64_t n,
+                       cudaStream_t st);
 void launch_permute(const double* src, const int32_t* perm, int64_t n, double* dst,
                     cudaStream_t st);
 

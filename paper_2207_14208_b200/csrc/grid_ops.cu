@@ -860,6 +860,104 @@ void launch_scale(double* u, int64_t n, double s, cudaStream_t st) {
   scale_kernel<<<grid_for(n, 256), 256, 0, st>>>(u, n, s);
 }
 
+// NumPy pairwise sum of squares (the reference's (r**2).sum(), solver.py:138;
+// SURVEY Appendix A.3) over a compacted vector, evaluated as its own tree:
+// leaves of <= 128 consecutive elements (8 strided accumulators, fixed
+// combine; < 8 elements: a left-to-right chain from -0), then every internal
+// node = left + right, one launch per tree height.  The leaf segments and
+// node list come from the host (the tree depends only on the length).
+// leaf over the internal nodes of grid positions [start, end) in order
+__global__ void l2_leaf_scan_kernel(const uint8_t* __restrict__ lab, const double* __restrict__ r,
+                                    const int64_t* __restrict__ start, const int64_t* __restrict__ end,
+                                    const int32_t* __restrict__ len, int64_t nleaves, double* __restrict__ vals) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nleaves) return;
+  const int n = len[t];
+  double acc[8];
+  double res = -0.0;
+  int i = 0;
+  const int body = n - (n % 8);
+  for (int64_t p = start[t]; p < end[t]; ++p) {
+    if (lab[p] != INTERNAL) continue;
+    const double v = r[p];
+    const double sq = v * v;
+    if (n < 8) {
+      res = res + sq;
+    } else if (i < 8) {
+      acc[i] = sq;
+    } else if (i < body) {
+      acc[i & 7] = acc[i & 7] + sq;
+    } else {
+      if (i == body) res = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      res = res + sq;
+    }
+    ++i;
+  }
+  if (n >= 8 && body == n) res = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  vals[t] = res;
+}
+
+// leaf over entries [off, off+len) of the lexicographic ghost list (value x[pos[slot[i]]])
+__global__ void l2_leaf_list_kernel(const double* __restrict__ x, const int64_t* __restrict__ pos,
+                                    const int32_t* __restrict__ slot, const int64_t* __restrict__ off,
+                                    const int32_t* __restrict__ len, int64_t nleaves, double* __restrict__ vals) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nleaves) return;
+  const int n = len[t];
+  const int64_t o = off[t];
+  double res = -0.0;
+  if (n < 8) {
+    for (int i = 0; i < n; ++i) {
+      const double v = x[pos[slot[o + i]]];
+      res = res + v * v;
+    }
+  } else {
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double v = x[pos[slot[o + j]]];
+      acc[j] = v * v;
+    }
+    const int body = n - (n % 8);
+    for (int i = 8; i < body; i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double v = x[pos[slot[o + i + j]]];
+        acc[j] = acc[j] + v * v;
+      }
+    res = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    for (int i = body; i < n; ++i) {
+      const double v = x[pos[slot[o + i]]];
+      res = res + v * v;
+    }
+  }
+  vals[t] = res;
+}
+
+// internal nodes of one tree height: vals[dst[k]] = vals[a[k]] + vals[b[k]]
+__global__ void l2_combine_kernel(double* __restrict__ vals, const int32_t* __restrict__ a,
+                                  const int32_t* __restrict__ b, const int32_t* __restrict__ dst, int64_t n) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < n) vals[dst[k]] = vals[a[k]] + vals[b[k]];
+}
+
+void launch_l2_leaves_scan(const uint8_t* lab, const double* r, const int64_t* start, const int64_t* end,
+                           const int32_t* len, int64_t nleaves, double* vals, cudaStream_t st) {
+  if (nleaves > 0)
+    l2_leaf_scan_kernel<<<(unsigned)((nleaves + 127) / 128), 128, 0, st>>>(lab, r, start, end, len, nleaves, vals);
+}
+
+void launch_l2_leaves_list(const double* x, const int64_t* pos, const int32_t* slot, const int64_t* off,
+                           const int32_t* len, int64_t nleaves, double* vals, cudaStream_t st) {
+  if (nleaves > 0)
+    l2_leaf_list_kernel<<<(unsigned)((nleaves + 127) / 128), 128, 0, st>>>(x, pos, slot, off, len, nleaves, vals);
+}
+
+void launch_l2_combine(double* vals, const int32_t* a, const int32_t* b, const int32_t* dst, int64_t n,
+                       cudaStream_t st) {
+  if (n > 0) l2_combine_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(vals, a, b, dst, n);
+}
+
 // Host-layout <-> padded device layout: row r of length n sits at
 // r * n in the contiguous (host) array and at r * P + OFF on the device.
 // The host copy is one contiguous DMA into a staging buffer; these kernels

@@ -20,6 +20,8 @@ Drop-in for /root/reference/pkg/src/ghostmg/solver.py:
   the reference at round-off level (bounded in tests/test_gpu_parity.py).
 """
 
+import math
+
 import numpy as np
 from scipy.sparse.linalg import splu
 
@@ -62,7 +64,7 @@ class DeviceHierarchy:
         else:
             coarse_mode = 0
         self.ctx.set_cycle(smoother.nu1, smoother.nu2, cycle.gamma, coarse_mode,
-                           cycle.coarse_sweeps, 0)
+                           cycle.coarse_sweeps, 1 if cycle.norm == NORM_L2 else 0)
         self._lu = None
         if coarse_mode == 0:
             self.ctx.set_coarse_callback(self._coarse)
@@ -181,8 +183,6 @@ class MultigridSolver(CycleDriver):
         return self
 
     def _init_device(self, device, coarse_backend):
-        if self.cycle_cfg.norm == NORM_L2:
-            raise NotImplementedError("norm='l2' is not implemented on the B200 path yet")
         self.coarse_backend = coarse_backend
         self.device = DeviceHierarchy(self.plans, self.smoother, self.cycle_cfg, device,
                                       coarse_backend)
@@ -216,6 +216,9 @@ class MultigridSolver(CycleDriver):
 
     def _residual_norm(self):
         m_int, m_g = self.ctx.residual_parts(0)
+        if self.cycle_cfg.norm == NORM_L2:
+            # device sums of squares, NumPy's pairwise order (solver.py:138)
+            return math.sqrt(float(m_int + m_g))
         p = self.plans[0]
         m = m_int if p.n_internal else 0.0
         if p.n_ghosts:
