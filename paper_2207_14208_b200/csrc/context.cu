@@ -139,6 +139,8 @@ struct gmg_ctx {
   int gs_variant = 0;          // GS implementation variant (GMG_GS_VARIANT, experiments)
   int halo_multi = -1;         // GS halo loader: -1 by level size, 0 two-batch, 1 multi-batch (GMG_GS_HALO)
   int ghost_bps = 8;           // ghost sweep: CTAs per SM (GMG_GHOST_BPS)
+  bool ghost_raw_only = true;  // ghost sweep: new values only in the pairs until a write-back launch, so
+                               // only read-after-write dependencies are waited for (GMG_GHOST_RAW=0: old scheme)
   bool ghost_levels = false;   // ghost sweep: level-synchronous kernel (GMG_GHOST_LEVELS=1; slower)
   int ghost_backoff = 300;     // ghost sweep: poll back-off ns (GMG_GHOST_BACKOFF)
   int gs_sleep[4] = {500, 500, 20, 200};  // GS loader / writer back-off (ns), GMG_GS_SLEEP=u,f,h,w  // one launch per ghost batch instead of the persistent sweep
@@ -494,8 +496,12 @@ int op_ghost_sweep(gmg_ctx* ctx, DevLevel& l) {
     gtrace = l.ghtrace;
   }
   launch_ghost_persistent(a, l.u, l.dep_off, l.dep, l.vmask, l.gpair, l.gctr, ctx->sms, ctx->ghost_bps,
-                          ctx->ghost_backoff, gtrace, ctx->stream);
+                          ctx->ghost_backoff, gtrace, ctx->ghost_raw_only, ctx->stream);
   ctx->launches++;
+  if (ctx->ghost_raw_only) {
+    launch_ghost_writeback(a, l.gpair, l.u, ctx->stream);
+    ctx->launches++;
+  }
   return 0;
 }
 
@@ -867,6 +873,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_VARIANT")) ctx->gs_variant = atoi(e);
   if (const char* e = getenv("GMG_GS_HALO")) ctx->halo_multi = atoi(e);
   if (const char* e = getenv("GMG_GHOST_BPS")) ctx->ghost_bps = std::max(1, atoi(e));
+  if (const char* e = getenv("GMG_GHOST_RAW")) ctx->ghost_raw_only = e[0] != '0';
   if (const char* e = getenv("GMG_GHOST_LEVELS")) ctx->ghost_levels = e[0] == '1';
   if (const char* e = getenv("GMG_GHOST_BACKOFF")) ctx->ghost_backoff = atoi(e);
   if (const char* e = getenv("GMG_GS_SLEEP"))
@@ -1009,8 +1016,10 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
         if (jg < 0 || jg == i) continue;
         if (jg < i)
           edges.push_back({l2s[i], l2s[jg], j});  // i reads jg's new value
-        else
+        else if (!ctx->ghost_raw_only)
           edges.push_back({l2s[jg], l2s[i], -1});  // jg must not change before i read it
+        // (with ghost_raw_only the persistent sweep leaves u untouched until its
+        // write-back, so later ghosts' old values stay readable: no WAR edges)
       }
     }
     std::sort(edges.begin(), edges.end(), [](const Edge& x, const Edge& y) {

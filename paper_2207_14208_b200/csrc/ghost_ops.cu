@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(256) ghost_persistent_kernel(GhostArgs a, doub
                                                                const int32_t* __restrict__ dep,
                                                                const uint32_t* __restrict__ vmask,
                                                                double* pair, int* cursor, int backoff,
-                                                               long long* gtrace) {
+                                                               long long* gtrace, bool defer) {
   constexpr int M = D == 3 ? 27 : 9;
   const int lane = threadIdx.x & 31;
   const int64_t nchunks = a.ng / 32;
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) ghost_persistent_kernel(GhostArgs a, doub
       if (gtrace) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tg1));
       const double dot = blas_ddot<M>(x, y);
       const double nv = uo + dt * (gv - dot);
-      __stcg(u + node, nv);
+      if (!defer) __stcg(u + node, nv);  // defer: u keeps the old value until the write-back
       st_pair(pair + 2 * s, nv);
     }
     if (gtrace) {
@@ -219,17 +219,31 @@ void launch_ghost_levels(const GhostArgs& a, double* u, const int64_t* boff, int
 
 void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_off, const int32_t* dep,
                              const uint32_t* vmask, double* pair, int* cursor, int sms, int blocks_per_sm,
-                             int backoff, long long* gtrace, cudaStream_t st) {
+                             int backoff, long long* gtrace, bool defer, cudaStream_t st) {
   const int64_t warps = a.ng / 32;
   int blocks = (int)std::min<int64_t>((warps + 7) / 8, (int64_t)sms * blocks_per_sm);
   if (blocks < 1) blocks = 1;
   if (a.g.d == 3)
-    ghost_persistent_kernel<3><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace);
+    ghost_persistent_kernel<3><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace,
+                                                       defer);
   else
-    ghost_persistent_kernel<2><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace);
+    ghost_persistent_kernel<2><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace,
+                                                       defer);
 }
 
 
+
+// Write-back of a deferred sweep: u[ghost] = its new value from the pairs.
+__global__ void ghost_writeback_kernel(GhostArgs a, const double* __restrict__ pair, double* __restrict__ u) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= a.ng) return;
+  const int64_t node = a.node[s];
+  if (node >= 0) u[node] = pair[2 * s];
+}
+
+void launch_ghost_writeback(const GhostArgs& a, const double* pair, double* u, cudaStream_t st) {
+  if (a.ng > 0) ghost_writeback_kernel<<<(unsigned)((a.ng + 255) / 256), 256, 0, st>>>(a, pair, u);
+}
 
 void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, double* pair, cudaStream_t st) {
   if (hi <= lo) return;

@@ -74,7 +74,8 @@ void launch_ghost_levels(const GhostArgs& a, double* u, const int64_t* boff, int
                          cudaStream_t st);
 void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_off, const int32_t* dep,
                              const uint32_t* vmask, double* pair, int* cursor, int sms, int blocks_per_sm,
-                             int backoff, long long* gtrace, cudaStream_t st);
+                             int backoff, long long* gtrace, bool defer, cudaStream_t st);
+void launch_ghost_writeback(const GhostArgs& a, const double* pair, double* u, cudaStream_t st);
 void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,
                            unsigned long long* maxbits, cudaStream_t st);
 void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,
