@@ -67,6 +67,9 @@ __device__ __forceinline__ double wait_pair(const double* p, int backoff) {
   return v.x;
 }
 
+#ifndef GHOST_MINB
+#define GHOST_MINB 1
+#endif
 // The whole ghost sweep in one launch, ordered by the sweep DAG instead of
 // batch barriers: warps claim 32-slot chunks in slot order (batch, lex).  A
 // ghost prefetches its weights and all 3^d stencil values, then takes the
@@ -78,7 +81,7 @@ __device__ __forceinline__ double wait_pair(const double* p, int backoff) {
 // deadlock, and each ghost sees the same values as in the reference's
 // lexicographic loop.  Pairs and the chunk cursor are zeroed before the launch.
 template <int D>
-__global__ void __launch_bounds__(256) ghost_persistent_kernel(GhostArgs a, double* __restrict__ u,
+__global__ void __launch_bounds__(256, GHOST_MINB) ghost_persistent_kernel(GhostArgs a, double* __restrict__ u,
                                                                const int32_t* __restrict__ dep_off,
                                                                const int32_t* __restrict__ dep,
                                                                const uint32_t* __restrict__ vmask,
