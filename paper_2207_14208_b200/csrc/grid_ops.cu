@@ -171,7 +171,8 @@ __global__ void __launch_bounds__(128) residual_rows3_kernel(Geom g, const uint8
 // of RM_S slots, RM_S - 1 planes ahead, so u is read from L2 about once
 // (+ halo) instead of once per stencil neighbour.  Same arithmetic order as
 // residual_interior_kernel.  r == nullptr: only the maximum (norm pass).
-constexpr int RM_TJ = 8, RM_TK = 64, RM_S = 5, RM_UW = RM_TK + 4;  // u row: [pad, k0-1, k0 .. k0+63, k0+64, pad]
+constexpr int RM_TK = 64, RM_UW = RM_TK + 4;  // u row: [pad, k0-1, k0 .. k0+63, k0+64, pad]
+template <int RM_TJ, int RM_S>
 struct __align__(16) ResMarchSmem {
   double u[RM_S][RM_TJ + 2][RM_UW];
   double f[RM_S][RM_TJ][RM_TK];
@@ -196,14 +197,14 @@ __device__ __forceinline__ void cpa_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <bool WRITE>
+template <bool WRITE, int RM_TJ, int RM_S>
 __global__ void __launch_bounds__(RM_TJ * 32) residual_march3_kernel(Geom g, const uint8_t* __restrict__ lab,
                                                                      const double* __restrict__ u,
                                                                      const double* __restrict__ f,
                                                                      double* __restrict__ r,
                                                                      unsigned long long* maxbits) {
   extern __shared__ __align__(16) unsigned char rm_raw[];
-  ResMarchSmem& S = *reinterpret_cast<ResMarchSmem*>(rm_raw);
+  ResMarchSmem<RM_TJ, RM_S>& S = *reinterpret_cast<ResMarchSmem<RM_TJ, RM_S>*>(rm_raw);
   const int N = (int)g.N;
   const int k0 = 1 + (int)blockIdx.x * RM_TK, j0 = 1 + (int)blockIdx.y * RM_TJ;
   const int per = (N - 1 + (int)gridDim.z - 1) / (int)gridDim.z;
@@ -314,21 +315,38 @@ void launch_residual_interior(const Geom& g, const uint8_t* labels, const double
                               const double* f, double* r, unsigned long long* maxbits,
                               cudaStream_t st) {
   if (g.d == 3 && !getenv("GMG_RES_ROWS")) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(residual_march3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(ResMarchSmem));
-      cudaFuncSetAttribute(residual_march3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(ResMarchSmem));
-      attr = true;
+    // tile 8 rows x 64 columns, 5-slot ring (4 CTAs per SM); GMG_RES_TILE=16: 16 rows, 2 CTAs per SM (on par)
+    static int tj_sel = -1;
+    if (tj_sel < 0) {
+      const char* e = getenv("GMG_RES_TILE");
+      tj_sel = e ? atoi(e) : 8;
+      cudaFuncSetAttribute(residual_march3_kernel<true, 8, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ResMarchSmem<8, 5>));
+      cudaFuncSetAttribute(residual_march3_kernel<false, 8, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ResMarchSmem<8, 5>));
+      cudaFuncSetAttribute(residual_march3_kernel<true, 16, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ResMarchSmem<16, 5>));
+      cudaFuncSetAttribute(residual_march3_kernel<false, 16, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ResMarchSmem<16, 5>));
     }
-    const int64_t tk = (g.N - 1 + RM_TK - 1) / RM_TK, tj = (g.N - 1 + RM_TJ - 1) / RM_TJ;
-    const int64_t segs = std::max<int64_t>(1, std::min<int64_t>((g.N - 1) / 4, 148 * 4 / (tk * tj)));
+    const int TJ = tj_sel == 8 ? 8 : 16;
+    const int per_sm = TJ == 8 ? 4 : 2;
+    const int64_t tk = (g.N - 1 + RM_TK - 1) / RM_TK, tj = (g.N - 1 + TJ - 1) / TJ;
+    const int64_t segs = std::max<int64_t>(1, std::min<int64_t>((g.N - 1) / 4, 148 * per_sm / (tk * tj)));
     dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)segs);
-    if (r)
-      residual_march3_kernel<true><<<grid, RM_TJ * 32, sizeof(ResMarchSmem), st>>>(g, labels, u, f, r, maxbits);
-    else
-      residual_march3_kernel<false><<<grid, RM_TJ * 32, sizeof(ResMarchSmem), st>>>(g, labels, u, f, r, maxbits);
+    if (TJ == 8) {
+      if (r)
+        residual_march3_kernel<true, 8, 5><<<grid, 8 * 32, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits);
+      else
+        residual_march3_kernel<false, 8, 5><<<grid, 8 * 32, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits);
+    } else {
+      if (r)
+        residual_march3_kernel<true, 16, 5><<<grid, 16 * 32, sizeof(ResMarchSmem<16, 5>), st>>>(g, labels, u, f, r,
+                                                                                               maxbits);
+      else
+        residual_march3_kernel<false, 16, 5><<<grid, 16 * 32, sizeof(ResMarchSmem<16, 5>), st>>>(g, labels, u, f, r,
+                                                                                                maxbits);
+    }
   } else if (g.d == 3 && getenv("GMG_RES_STREAM")) {
     dim3 grid((unsigned)((g.N - 1 + RT_K - 1) / RT_K), (unsigned)((g.N - 1 + RT_J - 1) / RT_J));
     residual_stream3_kernel<<<grid, 256, 0, st>>>(g, labels, u, f, r, maxbits);
