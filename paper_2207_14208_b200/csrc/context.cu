@@ -73,6 +73,7 @@ struct DevLevel {
   double *bv0 = nullptr, *bv1 = nullptr;
   // Gauss-Seidel tasks
   int2* tasks = nullptr;
+  uint8_t* tempty = nullptr;  // per task (list order): no internal node
   int ntasks = 0, B1 = 1, Bn = 1, C = 1;
   uint32_t* imask = nullptr;  // streaming GS: internal bitmask per (line, chunk)
   uint32_t* imask2 = nullptr; // diagonal GS (3-D): masks per (plane, block, pseudo-line)
@@ -212,7 +213,7 @@ void free_level(DevLevel& l) {
   free_tree(l.l2g);
   void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
-                  l.bscratch, l.tasks, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
+                  l.bscratch, l.tasks, l.tempty, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
                   l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off,
                   l.bfixpos, l.bnbr, l.bv0, l.bv1, l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g,
                   l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part};  // ticket lives in progress
@@ -440,6 +441,7 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
   a.u = l.u;
   a.f = l.f;
   a.tasks = l.tasks;
+  a.empty = l.diag_gs ? l.tempty : nullptr;
   a.ntasks = l.ntasks;
   a.ticket = l.ticket;
   a.progress = l.progress;
@@ -1120,6 +1122,7 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     l.B1 = 1;
     l.Bn = 1;
   }
+  std::vector<uint32_t> empty_im;  // copy of the internal-node bitmask for the empty-task test
   if (l.stream_gs) {
     // bit j of word (line, c) <=> node k = 1 + 32c + j of that line is internal
     const int64_t n = N + 1;
@@ -1132,6 +1135,7 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
         if (row[k] == INTERNAL) im[(size_t)(ln * l.Cm + (k - 1) / 32)] |= 1u << ((k - 1) % 32);
     }
     if (upload(ctx, &l.imask, im.data(), lines * l.Cm)) return -1;
+    if (l.diag_gs) empty_im = im;
     if (l.ws_gs) {
       const uint64_t P = (uint64_t)l.g.P;
       if (!make_map(&l.maps.u, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, l.u, P, (uint64_t)l.g.rows, P * 8, 36, 8) ||
@@ -1173,7 +1177,29 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
       const int b = s - c;
       if (b >= 0 && b < l.Bn) tasks.push_back(make_int2(c, b));
     }
+  // tasks without internal nodes (sparse domains): the diagonal kernel
+  // publishes them as done at once -- their columns never change
+  std::vector<uint8_t> tempty(tasks.size(), 0);
+  if (l.diag_gs && !empty_im.empty()) {
+    for (size_t t = 0; t < tasks.size(); ++t) {
+      const int c = tasks[t].x, b = tasks[t].y;
+      bool any = false;
+      if (d == 3) {
+        const int64_t rowbase = 1 + (int64_t)l.B1 * b;
+        const int64_t Rb = std::min<int64_t>(l.B1, N - 1 - l.B1 * (int64_t)b);
+        for (int64_t p = 1; p <= N - 1 && !any; ++p)
+          for (int64_t r = 0; r < Rb && !any; ++r)
+            any = empty_im[(size_t)((p * (N + 1) + rowbase + r) * l.Cm + c)] != 0;
+      } else {
+        for (int64_t row = 0; row <= N && !any; ++row) any = empty_im[(size_t)(row * l.Cm + c)] != 0;
+      }
+      tempty[t] = any ? 0 : 1;
+    }
+  }
   l.ntasks = (int)tasks.size();
+  if (l.tempty) cudaFree(l.tempty);
+  l.tempty = nullptr;
+  if (upload(ctx, &l.tempty, tempty.data(), (int64_t)tempty.size())) return -1;
   // progress words: 16 B per task (the TMA-store path writes them with bulk copies);
   // the older kernels use the first C * Bn ints
   if (upload(ctx, &l.tasks, tasks.data(), l.ntasks) || dalloc(ctx, &l.progress, 4 * l.C * l.Bn + 4))

@@ -13,6 +13,7 @@ struct GsArgs {
   double* u;
   const double* f;
   const int2* tasks;  // (chunk c, block b) in wavefront order
+  const uint8_t* empty;  // gs_diag: task without internal nodes (published as done at once), or null
   int ntasks;
   int* ticket;
   int* progress;      // [C * Bn] completed lines per task

@@ -306,6 +306,16 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
     if (tid >= a.ntasks) return;
     const int2 tk = a.tasks[tid];
     const int c = tk.x, b = tk.y;
+    if (a.empty && a.empty[tid]) {
+      // no internal node in this chunk x block: nothing changes, neighbours
+      // read its columns / rows as they are
+      if (threadIdx.x == 0) {
+        const int nl = D == 3 ? (N - 1) * PL : ((N + 1 + 7) & ~7);
+        st_relaxed(a.progress + 4 * (c * a.Bn + b), nl);
+      }
+      __syncthreads();
+      continue;
+    }
     const int k0 = 1 + 32 * c;
     Lines ln;
     ln.d = D;
