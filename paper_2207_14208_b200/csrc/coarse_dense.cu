@@ -91,14 +91,18 @@ __global__ void __launch_bounds__(256) gemv_rect_partial_kernel(const double* __
     const int64_t row = r0 + rr;
     if (row >= m) break;
     const double* a = A + row * k + c0;
-    double s0 = 0.0, s1 = 0.0;
+    // four independent accumulators (4 loads per lane in flight), fixed order
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int j = lane;
-    for (; j + 32 < len; j += 64) {
-      s0 = __fma_rn(__ldcs(a + j), xs[j], s0);
-      s1 = __fma_rn(__ldcs(a + j + 32), xs[j + 32], s1);
+    for (; j + 96 < len; j += 128) {
+      const double a0 = __ldcs(a + j), a1 = __ldcs(a + j + 32), a2 = __ldcs(a + j + 64), a3 = __ldcs(a + j + 96);
+      s0 = __fma_rn(a0, xs[j], s0);
+      s1 = __fma_rn(a1, xs[j + 32], s1);
+      s2 = __fma_rn(a2, xs[j + 64], s2);
+      s3 = __fma_rn(a3, xs[j + 96], s3);
     }
-    if (j < len) s0 = __fma_rn(__ldcs(a + j), xs[j], s0);
-    double s = s0 + s1;
+    for (; j < len; j += 32) s0 = __fma_rn(__ldcs(a + j), xs[j], s0);
+    double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) part[(int64_t)ch * m + row] = s;
