@@ -108,6 +108,11 @@ int gmg_set_coarse_inverse(gmg_ctx *ctx, int64_t n, const double *inv, int on_de
 int gmg_set_coarse_nd(gmg_ctx *ctx, int64_t n, int64_t na, int64_t nb, int64_t ns, const int32_t *perm,
                       const double *aai, const double *bbi, const double *g, const double *w,
                       const double *si, int on_device);
+/* Optional: the separator rows' coupling [A_SA A_SB] as host CSR (ns rows,
+ * columns in the permuted [A | B] order); the reduced right-hand side is then
+ * b_S - C [AAi b_A; BBi b_B] with a sparse product instead of the dense G. */
+int gmg_set_coarse_nd_coupling(gmg_ctx *ctx, int64_t ns, int64_t nab, const int64_t *rowptr,
+                               const int32_t *col, const double *val);
 
 /* Host <-> device copies of a level vector (see enum gmg_vector). */
 int gmg_set_vector(gmg_ctx *ctx, int level, int which, const double *host);

@@ -41,6 +41,7 @@ SIGNATURES = {
     "gmg_set_coarse_callback": (_i, [_p, COARSE_CB, _p]),
     "gmg_set_coarse_inverse": (_i, [_p, _i64, _p, _i]),
     "gmg_set_coarse_nd": (_i, [_p, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _i]),
+    "gmg_set_coarse_nd_coupling": (_i, [_p, _i64, _i64, _p, _p, _p]),
     "gmg_set_vector": (_i, [_p, _i, _i, _p]),
     "gmg_get_vector": (_i, [_p, _i, _i, _p]),
     "gmg_device_pointer": (_p, [_p, _i, _i]),
@@ -170,6 +171,13 @@ class Context:
         perm = np.ascontiguousarray(perm, dtype=np.int32)
         self.check(self.lib.gmg_set_coarse_nd(self.ctx, n, na, nb, ns, ptr(perm), aai, bbi, g, w, si,
                                               1 if on_device else 0))
+
+    def set_coarse_nd_coupling(self, ns, nab, rowptr, col, val):
+        """Sparse separator coupling (host CSR) for the nested-dissection solve."""
+        rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+        col = np.ascontiguousarray(col, dtype=np.int32)
+        val = np.ascontiguousarray(val, dtype=np.float64)
+        self.check(self.lib.gmg_set_coarse_nd_coupling(self.ctx, ns, nab, ptr(rowptr), ptr(col), ptr(val)))
 
     def set_stream(self, stream_handle):
         self.check(self.lib.gmg_set_stream(self.ctx, stream_handle))

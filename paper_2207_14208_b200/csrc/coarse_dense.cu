@@ -118,6 +118,27 @@ __global__ void gemv_rect_reduce_kernel(const double* __restrict__ part, int64_t
   y[i] = y0 ? y0[i] - s : s;
 }
 
+// t[i] = y0[i] - sum_k val[k] * x[col[k]] over row i of a CSR matrix (one
+// warp per row, fixed shuffle tree): the separator coupling A_S,AB applied to
+// the half solves, instead of the dense G = A_S,AB blkdiag(AAi, BBi).
+__global__ void csr_residual_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                    const double* __restrict__ val, const double* __restrict__ x,
+                                    const double* __restrict__ y0, int64_t m, double* __restrict__ t) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  double s = 0.0;
+  for (int64_t k = rowptr[row] + lane; k < rowptr[row + 1]; k += 32) s = __fma_rn(val[k], x[col[k]], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) t[row] = y0[row] - s;
+}
+
+void launch_csr_residual(const int64_t* rowptr, const int32_t* col, const double* val, const double* x,
+                         const double* y0, int64_t m, double* t, cudaStream_t st) {
+  if (m > 0) csr_residual_kernel<<<(unsigned)((m * 32 + 255) / 256), 256, 0, st>>>(rowptr, col, val, x, y0, m, t);
+}
+
 int gemv_rect_chunk(int64_t m, int64_t k) {
   // enough (row block, chunk) CTAs for ~4 per SM
   const int64_t rb = (m + GEMV_ROWS - 1) / GEMV_ROWS;

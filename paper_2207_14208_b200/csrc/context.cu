@@ -98,6 +98,9 @@ struct DevLevel {
   int64_t* nd_pos = nullptr;    // permuted position -> grid position
   double *nd_aai = nullptr, *nd_bbi = nullptr, *nd_g = nullptr, *nd_w = nullptr, *nd_si = nullptr;
   double *nd_b_ = nullptr, *nd_x = nullptr, *nd_t = nullptr, *nd_part = nullptr;
+  int64_t* nd_crow = nullptr;   // sparse separator coupling [A_SA A_SB] (CSR over [A | B] columns),
+  int32_t* nd_ccol = nullptr;   // used instead of the dense G when set
+  double* nd_cval = nullptr;
   PwTree l2i, l2g;  // l2 residual norm: internal nodes (lex order), ghosts (lex order)
   bool ready = false;
 };
@@ -216,7 +219,7 @@ void free_level(DevLevel& l) {
                   l.bscratch, l.tasks, l.tempty, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
                   l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off,
                   l.bfixpos, l.bnbr, l.bv0, l.bv1, l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g,
-                  l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part};  // ticket lives in progress
+                  l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part, l.nd_crow, l.nd_ccol, l.nd_cval};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -589,7 +592,10 @@ int coarse_solve(gmg_ctx* ctx, int li) {
     launch_permute(l.rhs_d, l.nd_perm, n, l.nd_b_, ctx->stream);
     launch_gemv_rect(l.nd_aai, l.nd_b_, na, na, l.nd_part, nullptr, l.nd_x, ctx->stream);
     launch_gemv_rect(l.nd_bbi, l.nd_b_ + na, nb, nb, l.nd_part, nullptr, l.nd_x + na, ctx->stream);
-    launch_gemv_rect(l.nd_g, l.nd_b_, ns, nab, l.nd_part, l.nd_b_ + nab, l.nd_t, ctx->stream);
+    if (l.nd_crow)
+      launch_csr_residual(l.nd_crow, l.nd_ccol, l.nd_cval, l.nd_x, l.nd_b_ + nab, ns, l.nd_t, ctx->stream);
+    else
+      launch_gemv_rect(l.nd_g, l.nd_b_, ns, nab, l.nd_part, l.nd_b_ + nab, l.nd_t, ctx->stream);
     launch_gemv_rect(l.nd_si, l.nd_t, ns, ns, l.nd_part, nullptr, l.nd_x + nab, ctx->stream);
     launch_gemv_rect(l.nd_w, l.nd_x + nab, nab, ns, l.nd_part, l.nd_x, l.nd_x, ctx->stream);
     launch_scatter(l.nd_pos, n, l.nd_x, l.u, ctx->stream);
@@ -1273,12 +1279,16 @@ int gmg_set_coarse_nd(gmg_ctx* ctx, int64_t n, int64_t na, int64_t nb, int64_t n
     return fail(ctx, "nested-dissection sizes do not match the coarsest level");
   cudaSetDevice(ctx->device);
   graph_reset(ctx);
-  void* old[] = {l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g, l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part};
+  void* old[] = {l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g, l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part,
+                 l.nd_crow, l.nd_ccol, l.nd_cval};
   for (void* p : old)
     if (p) cudaFree(p);
   l.nd_perm = nullptr;
   l.nd_pos = nullptr;
   l.nd_aai = l.nd_bbi = l.nd_g = l.nd_w = l.nd_si = l.nd_b_ = l.nd_x = l.nd_t = l.nd_part = nullptr;
+  l.nd_crow = nullptr;
+  l.nd_ccol = nullptr;
+  l.nd_cval = nullptr;
   l.nd_n = 0;
   const int64_t nab = na + nb;
   int64_t part = std::max({gemv_rect_part_size(na, na), gemv_rect_part_size(nb, nb), gemv_rect_part_size(ns, nab),
@@ -1305,6 +1315,26 @@ int gmg_set_coarse_nd(gmg_ctx* ctx, int64_t n, int64_t na, int64_t nb, int64_t n
   l.nd_a = na;
   l.nd_b = nb;
   l.nd_s = ns;
+  return 0;
+}
+
+int gmg_set_coarse_nd_coupling(gmg_ctx* ctx, int64_t ns, int64_t nab, const int64_t* rowptr, const int32_t* col,
+                               const double* val) {
+  DevLevel& l = ctx->L[ctx->nlevels - 1];
+  if (l.nd_n == 0 || ns != l.nd_s || nab != l.nd_a + l.nd_b) return fail(ctx, "set the nested-dissection blocks first");
+  cudaSetDevice(ctx->device);
+  graph_reset(ctx);
+  for (void* p : {(void*)l.nd_crow, (void*)l.nd_ccol, (void*)l.nd_cval})
+    if (p) cudaFree(p);
+  l.nd_crow = nullptr;
+  l.nd_ccol = nullptr;
+  l.nd_cval = nullptr;
+  const int64_t nnz = rowptr[ns];
+  for (int64_t k = 0; k < nnz; ++k)
+    if (col[k] < 0 || col[k] >= nab) return fail(ctx, "coupling column out of range");
+  if (upload(ctx, &l.nd_crow, rowptr, ns + 1) || upload(ctx, &l.nd_ccol, col, std::max<int64_t>(nnz, 1)) ||
+      upload(ctx, &l.nd_cval, val, std::max<int64_t>(nnz, 1)))
+    return -1;
   return 0;
 }
 

@@ -104,6 +104,8 @@ int gemv_chunks(int64_t n);
 void launch_gemv_rect(const double* A, const double* x, int64_t m, int64_t k, double* part, const double* y0,
                       double* y, cudaStream_t st);
 int64_t gemv_rect_part_size(int64_t m, int64_t k);
+void launch_csr_residual(const int64_t* rowptr, const int32_t* col, const double* val, const double* x,
+                         const double* y0, int64_t m, double* t, cudaStream_t st);
 void launch_repitch(const double* src, double* dst, int64_t rows, int64_t n, int64_t P, bool to_padded,
                     cudaStream_t st);
 void launch_l2_leaves_scan(const uint8_t* lab, const double* r, const int64_t* start, const int64_t* end,

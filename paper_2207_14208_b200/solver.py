@@ -140,6 +140,10 @@ class DeviceHierarchy:
         perm = np.concatenate([a, b, sep]).astype(np.int32)
         self.ctx.set_coarse_nd(len(perm), len(a), len(b), len(sep), perm, aai.data_ptr(), bbi.data_ptr(),
                                g.data_ptr(), w.data_ptr(), si.data_ptr(), True)
+        # the separator coupling, sparse, over the permuted [A | B] columns
+        coup = csr[sep][:, np.concatenate([a, b])].tocsr()
+        coup.sort_indices()
+        self.ctx.set_coarse_nd_coupling(len(sep), len(a) + len(b), coup.indptr, coup.indices, coup.data)
         self.nd_sizes = (len(a), len(b), len(sep))
         del aai, bbi, g, w, si, asp, bsp, sa, sb, wa, wb, ga, gb, schur
         torch.cuda.empty_cache()
