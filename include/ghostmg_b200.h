@@ -113,6 +113,19 @@ int gmg_set_coarse_nd(gmg_ctx *ctx, int64_t n, int64_t na, int64_t nb, int64_t n
  * b_S - C [AAi b_A; BBi b_B] with a sparse product instead of the dense G. */
 int gmg_set_coarse_nd_coupling(gmg_ctx *ctx, int64_t ns, int64_t nab, const int64_t *rowptr,
                                const int32_t *col, const double *val);
+/* General form of the coarse_mode-2 solve (takes precedence over both of the
+ * above): a program of dense / sparse products on a workspace of nwork
+ * doubles.  begin: perm[i] = rhs-order index of workspace entry i (the
+ * permuted rhs lands in [0, n)); dense: y = M x, or y = y0 - M x when
+ * y0_off >= 0 (M row-major m x k, host or device memory, copied); csr:
+ * y = y0 - C x (host CSR, m rows, columns < k); end: the solution (permuted
+ * order) is at [x_off, x_off + n).  Used for recursive nested dissection. */
+int gmg_coarse_prog_begin(gmg_ctx *ctx, int64_t n, const int32_t *perm, int64_t nwork);
+int gmg_coarse_prog_dense(gmg_ctx *ctx, int64_t m, int64_t k, const double *M, int on_device,
+                          int64_t x_off, int64_t y_off, int64_t y0_off);
+int gmg_coarse_prog_csr(gmg_ctx *ctx, int64_t m, int64_t k, const int64_t *rowptr, const int32_t *col,
+                        const double *val, int64_t x_off, int64_t y0_off, int64_t y_off);
+int gmg_coarse_prog_end(gmg_ctx *ctx, int64_t x_off);
 
 /* Host <-> device copies of a level vector (see enum gmg_vector). */
 int gmg_set_vector(gmg_ctx *ctx, int level, int which, const double *host);

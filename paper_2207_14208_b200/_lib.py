@@ -42,6 +42,10 @@ SIGNATURES = {
     "gmg_set_coarse_inverse": (_i, [_p, _i64, _p, _i]),
     "gmg_set_coarse_nd": (_i, [_p, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _i]),
     "gmg_set_coarse_nd_coupling": (_i, [_p, _i64, _i64, _p, _p, _p]),
+    "gmg_coarse_prog_begin": (_i, [_p, _i64, _p, _i64]),
+    "gmg_coarse_prog_dense": (_i, [_p, _i64, _i64, _p, _i, _i64, _i64, _i64]),
+    "gmg_coarse_prog_csr": (_i, [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64]),
+    "gmg_coarse_prog_end": (_i, [_p, _i64]),
     "gmg_set_vector": (_i, [_p, _i, _i, _p]),
     "gmg_get_vector": (_i, [_p, _i, _i, _p]),
     "gmg_device_pointer": (_p, [_p, _i, _i]),
@@ -178,6 +182,26 @@ class Context:
         col = np.ascontiguousarray(col, dtype=np.int32)
         val = np.ascontiguousarray(val, dtype=np.float64)
         self.check(self.lib.gmg_set_coarse_nd_coupling(self.ctx, ns, nab, ptr(rowptr), ptr(col), ptr(val)))
+
+    # -- coarse program (recursive nested dissection) ----------------------
+    def coarse_prog_begin(self, n, perm, nwork):
+        perm = np.ascontiguousarray(perm, dtype=np.int32)
+        self.check(self.lib.gmg_coarse_prog_begin(self.ctx, n, ptr(perm), nwork))
+
+    def coarse_prog_dense(self, m, k, dev_ptr, x_off, y_off, y0_off=-1):
+        self.check(self.lib.gmg_coarse_prog_dense(self.ctx, m, k, dev_ptr, 1, x_off, y_off, y0_off))
+
+    def coarse_prog_csr(self, C, x_off, y0_off, y_off):
+        C = C.tocsr()
+        C.sort_indices()
+        rowptr = np.ascontiguousarray(C.indptr, dtype=np.int64)
+        col = np.ascontiguousarray(C.indices, dtype=np.int32)
+        val = np.ascontiguousarray(C.data, dtype=np.float64)
+        self.check(self.lib.gmg_coarse_prog_csr(self.ctx, C.shape[0], C.shape[1], ptr(rowptr), ptr(col), ptr(val),
+                                                x_off, y0_off, y_off))
+
+    def coarse_prog_end(self, x_off):
+        self.check(self.lib.gmg_coarse_prog_end(self.ctx, x_off))
 
     def set_stream(self, stream_handle):
         self.check(self.lib.gmg_set_stream(self.ctx, stream_handle))

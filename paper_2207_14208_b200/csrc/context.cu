@@ -98,6 +98,22 @@ struct DevLevel {
   int64_t* nd_pos = nullptr;    // permuted position -> grid position
   double *nd_aai = nullptr, *nd_bbi = nullptr, *nd_g = nullptr, *nd_w = nullptr, *nd_si = nullptr;
   double *nd_b_ = nullptr, *nd_x = nullptr, *nd_t = nullptr, *nd_part = nullptr;
+  // general coarse program (recursive nested dissection): ops on a workspace
+  struct CoarseOp {
+    int kind;  // 0: y = [y0 -] M x (dense m x k), 1: y = y0 - C x (CSR m rows)
+    int64_t m, k, x_off, y_off, y0_off;
+    double* M;
+    int64_t* rowptr;
+    int32_t* col;
+    double* val;
+  };
+  std::vector<CoarseOp> cprog;
+  bool cprog_ready = false;
+  int64_t cprog_n = 0, cprog_x = 0, cprog_work = 0;
+  int32_t* cprog_perm = nullptr;
+  int64_t* cprog_pos = nullptr;
+  double *cprog_w = nullptr, *cprog_part = nullptr;
+  int64_t cprog_part_n = 0;
   int64_t* nd_crow = nullptr;   // sparse separator coupling [A_SA A_SB] (CSR over [A | B] columns),
   int32_t* nd_ccol = nullptr;   // used instead of the dense G when set
   double* nd_cval = nullptr;
@@ -211,7 +227,25 @@ void free_tree(PwTree& t) {
   t = PwTree();
 }
 
+void free_cprog(DevLevel& l) {
+  for (auto& op : l.cprog) {
+    void* p[] = {op.M, op.rowptr, op.col, op.val};
+    for (void* q : p)
+      if (q) cudaFree(q);
+  }
+  l.cprog.clear();
+  void* p[] = {l.cprog_perm, l.cprog_pos, l.cprog_w, l.cprog_part};
+  for (void* q : p)
+    if (q) cudaFree(q);
+  l.cprog_perm = nullptr;
+  l.cprog_pos = nullptr;
+  l.cprog_w = l.cprog_part = nullptr;
+  l.cprog_part_n = 0;
+  l.cprog_ready = false;
+}
+
 void free_level(DevLevel& l) {
+  free_cprog(l);
   free_tree(l.l2i);
   free_tree(l.l2g);
   void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
@@ -584,6 +618,24 @@ int coarse_solve(gmg_ctx* ctx, int li) {
   GMG_CHECK(ctx, cudaMemsetAsync(l.u, 0, sizeof(double) * (size_t)l.g.nodes, ctx->stream));
   if (ctx->coarse_mode == 1) return op_smooth(ctx, l, ctx->coarse_sweeps);
   const int64_t n = l.n_int + l.ng;
+  if (ctx->coarse_mode == 2 && l.cprog_ready && l.cprog_n == n) {
+    // recursive nested dissection: the uploaded op program on the workspace
+    launch_gather(l.active, l.n_int, l.f, l.lex2slot, l.ng, l.gval, l.rhs_d, ctx->stream);
+    launch_permute(l.rhs_d, l.cprog_perm, n, l.cprog_w, ctx->stream);
+    ctx->launches += 2;
+    for (const auto& op : l.cprog) {
+      double* w = l.cprog_w;
+      if (op.kind == 0)
+        launch_gemv_rect(op.M, w + op.x_off, op.m, op.k, l.cprog_part, op.y0_off >= 0 ? w + op.y0_off : nullptr,
+                         w + op.y_off, ctx->stream);
+      else
+        launch_csr_residual(op.rowptr, op.col, op.val, w + op.x_off, w + op.y0_off, op.m, w + op.y_off, ctx->stream);
+      ctx->launches += op.kind == 0 ? 2 : 1;
+    }
+    launch_scatter(l.cprog_pos, n, l.cprog_w + l.cprog_x, l.u, ctx->stream);
+    ctx->launches++;
+    return 0;
+  }
   if (ctx->coarse_mode == 2 && l.nd_n == n) {
     // x = A^-1 rhs by one level of nested dissection (5 GEMVs, ~60 % of the
     // dense inverse's bytes)
@@ -1335,6 +1387,81 @@ int gmg_set_coarse_nd_coupling(gmg_ctx* ctx, int64_t ns, int64_t nab, const int6
   if (upload(ctx, &l.nd_crow, rowptr, ns + 1) || upload(ctx, &l.nd_ccol, col, std::max<int64_t>(nnz, 1)) ||
       upload(ctx, &l.nd_cval, val, std::max<int64_t>(nnz, 1)))
     return -1;
+  return 0;
+}
+
+int gmg_coarse_prog_begin(gmg_ctx* ctx, int64_t n, const int32_t* perm, int64_t nwork) {
+  DevLevel& l = ctx->L[ctx->nlevels - 1];
+  if (!l.ready) return fail(ctx, "coarsest level not set");
+  if (n != l.n_int + l.ng || nwork < 2 * n) return fail(ctx, "coarse program sizes do not match the coarsest level");
+  cudaSetDevice(ctx->device);
+  graph_reset(ctx);
+  free_cprog(l);
+  std::vector<int64_t> act((size_t)n), pos((size_t)n);
+  GMG_CHECK(ctx, cudaMemcpy(act.data(), l.active, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < n; ++i) {
+    if (perm[i] < 0 || perm[i] >= n) return fail(ctx, "coarse program permutation out of range");
+    pos[i] = act[perm[i]];
+  }
+  if (upload(ctx, &l.cprog_perm, perm, n) || upload(ctx, &l.cprog_pos, pos.data(), n) ||
+      dalloc(ctx, &l.cprog_w, nwork))
+    return -1;
+  GMG_CHECK(ctx, cudaMemset(l.cprog_w, 0, sizeof(double) * (size_t)nwork));
+  l.cprog_n = n;
+  l.cprog_work = nwork;
+  return 0;
+}
+
+int gmg_coarse_prog_dense(gmg_ctx* ctx, int64_t m, int64_t k, const double* M, int on_device, int64_t x_off,
+                          int64_t y_off, int64_t y0_off) {
+  DevLevel& l = ctx->L[ctx->nlevels - 1];
+  if (!l.cprog_w) return fail(ctx, "gmg_coarse_prog_begin first");
+  auto in = [&](int64_t o, int64_t len) { return o >= 0 && o + len <= l.cprog_work; };
+  if (m <= 0 || k <= 0 || !in(x_off, k) || !in(y_off, m) || (y0_off >= 0 && !in(y0_off, m)))
+    return fail(ctx, "coarse program op out of the workspace");
+  DevLevel::CoarseOp op{};
+  op.kind = 0;
+  op.m = m, op.k = k, op.x_off = x_off, op.y_off = y_off, op.y0_off = y0_off;
+  if (dalloc(ctx, &op.M, m * k)) return -1;
+  GMG_CHECK(ctx, cudaMemcpy(op.M, M, sizeof(double) * (size_t)(m * k),
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+  const int64_t part = gemv_rect_part_size(m, k);
+  if (part > l.cprog_part_n) {
+    if (l.cprog_part) cudaFree(l.cprog_part);
+    l.cprog_part = nullptr;
+    if (dalloc(ctx, &l.cprog_part, part)) return -1;
+    l.cprog_part_n = part;
+  }
+  l.cprog.push_back(op);
+  return 0;
+}
+
+int gmg_coarse_prog_csr(gmg_ctx* ctx, int64_t m, int64_t k, const int64_t* rowptr, const int32_t* col,
+                        const double* val, int64_t x_off, int64_t y0_off, int64_t y_off) {
+  DevLevel& l = ctx->L[ctx->nlevels - 1];
+  if (!l.cprog_w) return fail(ctx, "gmg_coarse_prog_begin first");
+  auto in = [&](int64_t o, int64_t len) { return o >= 0 && o + len <= l.cprog_work; };
+  if (m <= 0 || k <= 0 || !in(x_off, k) || !in(y_off, m) || !in(y0_off, m))
+    return fail(ctx, "coarse program op out of the workspace");
+  const int64_t nnz = rowptr[m];
+  for (int64_t q = 0; q < nnz; ++q)
+    if (col[q] < 0 || col[q] >= k) return fail(ctx, "coarse program CSR column out of range");
+  DevLevel::CoarseOp op{};
+  op.kind = 1;
+  op.m = m, op.k = k, op.x_off = x_off, op.y_off = y_off, op.y0_off = y0_off;
+  if (upload(ctx, &op.rowptr, rowptr, m + 1) || upload(ctx, &op.col, col, std::max<int64_t>(nnz, 1)) ||
+      upload(ctx, &op.val, val, std::max<int64_t>(nnz, 1)))
+    return -1;
+  l.cprog.push_back(op);
+  return 0;
+}
+
+int gmg_coarse_prog_end(gmg_ctx* ctx, int64_t x_off) {
+  DevLevel& l = ctx->L[ctx->nlevels - 1];
+  if (!l.cprog_w || x_off < 0 || x_off + l.cprog_n > l.cprog_work) return fail(ctx, "bad coarse program result");
+  l.cprog_x = x_off;
+  l.cprog_ready = true;
+  graph_reset(ctx);
   return 0;
 }
 

@@ -72,6 +72,8 @@ class DeviceHierarchy:
             self._upload_inverse()
 
     ND_MIN = 8192  # coarsest systems at least this large use the nested-dissection form
+    ND_DEPTH = 2   # dissection levels (leaves are dense inverses)
+    ND_LEAF = 2048  # subproblems smaller than this are not split further
 
     def _upload_inverse(self):
         """Invert the coarsest operator on the GPU (setup) and hand it to the
@@ -82,6 +84,8 @@ class DeviceHierarchy:
 
         A, active = coarsest_system(self.plans[-1])
         n = A.shape[0]
+        if n >= self.ND_MIN and self._upload_nd_program(A, active, depth=self.ND_DEPTH):
+            return
         if n >= self.ND_MIN and self._upload_nd(A, active):
             return
         dev = torch.device("cuda", self.device_index)
@@ -111,6 +115,86 @@ class DeviceHierarchy:
             if csr[a][:, b].nnz == 0 and csr[b][:, a].nnz == 0:
                 return a, b, sep
         return None
+
+    def _upload_nd_program(self, A, active, depth):
+        """Recursive nested dissection as a program of device products
+        (gmg_coarse_prog_*): a subproblem either is a leaf, x = inv(A_ii) b,
+        or splits by axis-0 planes into decoupled halves a, b and a separator
+        s: solve a and b, t = b_s - A_s,ab x_ab (sparse), x_s = Si t with Si the
+        inverse Schur complement, x_ab -= W x_s, W = blkdiag(inv(A_aa),
+        inv(A_bb)) A_ab,s.  Workspace: permuted rhs [0, n), solution [n, 2n),
+        separator temporaries after."""
+        import torch
+
+        csr = A.tocsr()
+        n = A.shape[0]
+        p = self.plans[-1]
+        per = (p.N + 1) ** (p.d - 1)
+        planes = np.asarray(active) // per
+        dev = torch.device("cuda", self.device_index)
+        ops = []
+        temp = [2 * n]
+
+        def dense(r, c):
+            return torch.from_numpy(csr[r][:, c].toarray()).to(dev)
+
+        def split(idx):
+            pl = planes[idx]
+            lo, hi = int(pl.min()), int(pl.max())
+            mid = (lo + hi) // 2
+            for w in range(1, max(2, (hi - lo) // 4)):
+                a, b = idx[pl < mid - w], idx[pl > mid + w]
+                s_ = idx[(pl >= mid - w) & (pl <= mid + w)]
+                if len(a) == 0 or len(b) == 0:
+                    return None
+                if csr[a][:, b].nnz == 0 and csr[b][:, a].nnz == 0:
+                    return a, b, s_
+            return None
+
+        def solve(idx, off, lvl):
+            sp = split(idx) if lvl > 0 and len(idx) >= self.ND_LEAF else None
+            if sp is None:
+                M = torch.linalg.inv(dense(idx, idx)).contiguous()
+                ops.append(("dense", M, len(idx), len(idx), off, n + off, -1))
+                return np.asarray(idx)
+            a, b, s_ = sp
+            oa = solve(a, off, lvl - 1)
+            ob = solve(b, off + len(a), lvl - 1)
+            ab = np.concatenate([oa, ob])
+            soff = off + len(ab)
+            ia = torch.linalg.inv(dense(oa, oa))
+            ib = torch.linalg.inv(dense(ob, ob))
+            W = torch.cat([ia @ dense(oa, s_), ib @ dense(ob, s_)], dim=0).contiguous()
+            del ia, ib
+            C = csr[s_][:, ab]
+            Cd = torch.from_numpy(C.toarray()).to(dev)
+            Si = torch.linalg.inv(dense(s_, s_) - Cd @ W).contiguous()
+            del Cd
+            t = temp[0]
+            temp[0] += len(s_)
+            ops.append(("csr", C, n + off, soff, t))
+            ops.append(("dense", Si, len(s_), len(s_), t, n + soff, -1))
+            ops.append(("dense", W, len(ab), len(s_), n + soff, n + off, n + off))
+            return np.concatenate([ab, s_])
+
+        root = split(np.arange(n))
+        if root is None:
+            return False
+        order = solve(np.arange(n), 0, depth)
+        torch.cuda.synchronize(dev)
+        self.ctx.coarse_prog_begin(n, order.astype(np.int32), temp[0])
+        for op in ops:
+            if op[0] == "dense":
+                _, M, m, k, xo, yo, y0 = op
+                self.ctx.coarse_prog_dense(m, k, M.data_ptr(), xo, yo, y0)
+            else:
+                _, C, xo, y0, yo = op
+                self.ctx.coarse_prog_csr(C, xo, y0, yo)
+        self.ctx.coarse_prog_end(n)
+        self.nd_sizes = tuple(op[2] for op in ops if op[0] == "dense")
+        ops.clear()
+        torch.cuda.empty_cache()
+        return True
 
     def _upload_nd(self, A, active):
         import torch
