@@ -21,6 +21,7 @@ Drop-in for /root/reference/pkg/src/ghostmg/solver.py:
 """
 
 import math
+import os
 
 import numpy as np
 from scipy.sparse.linalg import splu
@@ -84,7 +85,8 @@ class DeviceHierarchy:
 
         A, active = coarsest_system(self.plans[-1])
         n = A.shape[0]
-        if n >= self.ND_MIN and self._upload_nd_program(A, active, depth=self.ND_DEPTH):
+        depth = int(os.environ.get("GMG_ND_DEPTH", self.ND_DEPTH))
+        if n >= self.ND_MIN and depth > 0 and self._upload_nd_program(A, active, depth=depth):
             return
         if n >= self.ND_MIN and self._upload_nd(A, active):
             return
