@@ -763,8 +763,93 @@ __global__ void __launch_bounds__(256, 4) interp_add_kernel(Geom gf, const uint8
   }
 }
 
+// Quad variant: a thread takes padded positions 4q .. 4q+3 (fine columns
+// 4q-3 .. 4q, one 32-byte-aligned group): u as two 16-byte loads, the labels as
+// one 4-byte load, and per corner row only the three coarse columns 2q-2 .. 2q
+// the four nodes share (12 coarse loads for 4 nodes instead of 16).  Same
+// products and sums as interp_add_kernel.
+template <int D>
+__global__ void __launch_bounds__(256, 4) interp_add4_kernel(Geom gf, const uint8_t* __restrict__ lab_f,
+                                                          double* __restrict__ u, Geom gc,
+                                                          const double* __restrict__ e) {
+  constexpr int NC = 1 << D;
+  constexpr int NR = D == 3 ? 4 : 2;
+  const int nf = (int)gf.n;
+  const int hq = (int)(gf.P >> 2);  // quads per row
+  const int nq = (int)(gf.rows * hq);
+  for (int q0 = blockIdx.x * blockDim.x + threadIdx.x; q0 < nq; q0 += gridDim.x * blockDim.x) {
+    const int row = q0 / hq, m = q0 - row * hq;
+    const int ii = D == 3 ? row / nf : 0;
+    const int jj = D == 3 ? row - ii * nf : row;
+    const double2 ua = reinterpret_cast<const double2*>(u)[2 * q0];
+    const double2 ub = reinterpret_cast<const double2*>(u)[2 * q0 + 1];
+    const uint32_t L4 = reinterpret_cast<const uint32_t*>(lab_f)[q0];
+    const int oi = ii & 1, oj = jj & 1;
+    const int hi = ii >> 1, hj = jj >> 1;
+    const int c0 = max(2 * m - 2, 0) + (int)OFF, c1 = max(2 * m - 1, 0) + (int)OFF, c2 = 2 * m + (int)OFF;
+    double e0[NR], e1[NR], e2[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int cc0 = D == 3 ? r >> 1 : 0, cc1 = r & 1;
+      const int ri = hi + (oi ? cc0 : 0), rj = hj + (oj ? cc1 : 0);
+      const double* er = e + (D == 3 ? ((int64_t)ri * gc.n + rj) * gc.P : (int64_t)rj * gc.P);
+      e0[r] = er[c0];
+      e1[r] = er[c1];
+      e2[r] = er[c2];
+    }
+    double pa[NC], pb[NC], pc[NC], pd[NC];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int cc0 = D == 3 ? r >> 1 : 0, cc1 = r & 1;
+      const double wi = oi ? 0.5 : (cc0 == 0 ? 1.0 : 0.0);
+      const double wj = oj ? 0.5 : (cc1 == 0 ? 1.0 : 0.0);
+      const double wr = D == 3 ? (1.0 * wi) * wj : 1.0 * wj;
+      // k = 4m-3 (odd): columns 2m-2, 2m-1, weights 1/2, 1/2
+      pa[2 * r] = (wr * 0.5) * e0[r];
+      pa[2 * r + 1] = (wr * 0.5) * e1[r];
+      // k = 4m-2 (even): column 2m-1, weights 1, 0
+      pb[2 * r] = (wr * 1.0) * e1[r];
+      pb[2 * r + 1] = (wr * 0.0) * e1[r];
+      // k = 4m-1 (odd): columns 2m-1, 2m
+      pc[2 * r] = (wr * 0.5) * e1[r];
+      pc[2 * r + 1] = (wr * 0.5) * e2[r];
+      // k = 4m (even): column 2m
+      pd[2 * r] = (wr * 1.0) * e2[r];
+      pd[2 * r + 1] = (wr * 0.0) * e2[r];
+    }
+    auto upd = [](uint8_t L) { return L == INTERNAL || L == GHOST; };
+    const uint8_t la = L4 & 0xFF, lb = (L4 >> 8) & 0xFF, lc = (L4 >> 16) & 0xFF, ld = L4 >> 24;
+    if (upd(la) || upd(lb)) {
+      double2 o = ua;
+      if (upd(la)) o.x = ua.x + np_sum<NC>(pa);
+      if (upd(lb)) o.y = ua.y + np_sum<NC>(pb);
+      reinterpret_cast<double2*>(u)[2 * q0] = o;
+    }
+    if (upd(lc) || upd(ld)) {
+      double2 o = ub;
+      if (upd(lc)) o.x = ub.x + np_sum<NC>(pc);
+      if (upd(ld)) o.y = ub.y + np_sum<NC>(pd);
+      reinterpret_cast<double2*>(u)[2 * q0 + 1] = o;
+    }
+  }
+}
+
 void launch_interp_add(const Geom& gf, const uint8_t* lab_f, double* u_f, const Geom& gc,
                        const double* e_c, cudaStream_t st) {
+  static int quad = -1;
+  if (quad < 0) {
+    const char* env = getenv("GMG_INTERP4");
+    quad = env ? atoi(env) : 1;
+  }
+  if (quad) {
+    const int64_t nq = gf.rows * (gf.P / 4);
+    const unsigned blocks = grid_for(nq, 256, 148 * 8);
+    if (gf.d == 3)
+      interp_add4_kernel<3><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
+    else
+      interp_add4_kernel<2><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
+    return;
+  }
   const int64_t npairs = gf.rows * (gf.P / 2);
   const unsigned blocks = grid_for((npairs + PPT - 1) / PPT, 256, 148 * 8);
   if (gf.d == 3)
