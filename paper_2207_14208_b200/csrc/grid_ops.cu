@@ -467,6 +467,63 @@ __global__ void __launch_bounds__(256, 3) restrict_interior_kernel(Geom gf, cons
   }
 }
 
+// 3-D pair variant: a thread takes coarse columns K, K+1 (K odd) of a row;
+// per fine (plane, row) of their 3 x 3 block rows it loads the five fine
+// columns 2K-1 .. 2K+3 as two 16-byte loads and one 8-byte load (the nodes
+// share column 2K+1), the two masks as one 8-byte load.  Same weights and
+// summation order as restrict_interior_kernel.
+__global__ void __launch_bounds__(128) restrict_pair3_kernel(Geom gf, const double* __restrict__ r_f, Geom gc,
+                                                              const uint32_t* __restrict__ rmask,
+                                                              double* __restrict__ f_c) {
+  const int nc = (int)gc.n;
+  const int inner = nc - 2;
+  const int64_t nrows = (int64_t)inner * inner;
+  const int npairs = (inner + 1) / 2;
+  for (int64_t rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
+    const int I = (int)(rr / inner) + 1, J = (int)(rr % inner) + 1;
+    const int64_t crow = (int64_t)I * nc + J;
+    const int64_t frow = (int64_t)(2 * I) * gf.n + 2 * J;
+    for (int t = threadIdx.x; t < npairs; t += blockDim.x) {
+      const int K = 1 + 2 * t;
+      const bool two = K + 1 <= nc - 2;
+      const int64_t ic = crow * gc.P + K + OFF;  // even position: 8-byte aligned pair of masks
+      uint32_t m0, m1;
+      if (two) {
+        const uint2 mm = *reinterpret_cast<const uint2*>(rmask + ic);
+        m0 = mm.x, m1 = mm.y;
+      } else {
+        m0 = rmask[ic], m1 = 0u;
+      }
+      if (!((m0 | m1) & RM_COARSE)) continue;
+      double p0[27], p1[27];
+#pragma unroll
+      for (int pr = 0; pr < 9; ++pr) {  // (plane, row) of the block: e = 3 pr + column
+        const int dp = pr / 3 - 1, dr = pr % 3 - 1;
+        const double* rc = r_f + (frow + (int64_t)dp * gf.n + dr) * gf.P + 2 * K - 1 + OFF;  // column 2K-1
+        const double2 a = *reinterpret_cast<const double2*>(rc);
+        const double2 b = *reinterpret_cast<const double2*>(rc + 2);
+        const double c = two ? rc[4] : 0.0;
+        p0[3 * pr] = a.x, p0[3 * pr + 1] = a.y, p0[3 * pr + 2] = b.x;
+        p1[3 * pr] = b.x, p1[3 * pr + 1] = b.y, p1[3 * pr + 2] = c;
+      }
+      auto finish = [&](uint32_t m, double(&p)[27]) -> double {
+        if (m & RM_MIXED) {
+          const double dc = (double)__popc(m & ((1u << 27) - 1u));
+          const double w1 = 1.0 / dc;
+#pragma unroll
+          for (int e = 0; e < 27; ++e) p[e] = (((m >> e) & 1u) ? w1 : 0.0) * p[e];  // == (bit ? 1 : 0) / dc * p
+        } else {
+#pragma unroll
+          for (int e = 0; e < 27; ++e) p[e] = fw_w<3>(e) * p[e];
+        }
+        return np_sum<27>(p);
+      };
+      if (m0 & RM_COARSE) f_c[ic] = finish(m0, p0);
+      if (two && (m1 & RM_COARSE)) f_c[ic + 1] = finish(m1, p1);
+    }
+  }
+}
+
 // Fused interior residual + interior restriction (3-D):
 // residual_internal (smoothing.py:111-118) evaluated tile by tile and fed
 // straight into InteriorRestriction.apply (transfer.py:88-93); the fine
@@ -678,7 +735,15 @@ void launch_restrict_interior(const Geom& gf, const double* r_f, const Geom& gc,
   const int64_t inner = gc.n - 2;
   const int64_t nrows = gf.d == 3 ? inner * inner : inner;
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 8));
-  if (gf.d == 3)
+  static int pair = -1;
+  if (pair < 0) {
+    const char* env = getenv("GMG_RESTRICT_PAIR");
+    pair = env ? atoi(env) : 0;  // measured slower (371 vs 323 us at 512^3)
+  }
+  if (gf.d == 3 && pair) {
+    const unsigned b2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 16));
+    restrict_pair3_kernel<<<b2, 128, 0, st>>>(gf, r_f, gc, rmask, f_c);
+  } else if (gf.d == 3)
     restrict_interior_kernel<3><<<blocks, 256, 0, st>>>(gf, r_f, gc, rmask, f_c);
   else
     restrict_interior_kernel<2><<<blocks, 256, 0, st>>>(gf, r_f, gc, rmask, f_c);
