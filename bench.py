@@ -342,7 +342,7 @@ def run_b200(args, rank, world, local_rank):
             "config": {"workload": setup.name, "N": setup.grid.N, "levels": len(plans),
                        "dof": dof, "N_I": p0.n_internal, "N_G": p0.n_ghosts, "cycle": "V(2,1)",
                        "coarse": f"{setup.cycle.coarse_solver}:{args.coarse}", "parallelism": f"replicas{world}",
-                       "l2_flush": "not needed: every grid vector (1.08 GB) exceeds L2"},
+                       "l2_flush": f"not needed: every grid vector ({8 * p0.n_nodes / 1e9:.2f} GB) exceeds L2"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(), "breakdown_ms_per_cycle": breakdown, "setup": setup_times,
         }
