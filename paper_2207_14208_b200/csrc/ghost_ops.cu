@@ -68,7 +68,7 @@ __device__ __forceinline__ double wait_pair(const double* p, int backoff) {
 }
 
 #ifndef GHOST_MINB
-#define GHOST_MINB 1
+#define GHOST_MINB 2
 #endif
 // The whole ghost sweep in one launch, ordered by the sweep DAG instead of
 // batch barriers: warps claim 32-slot chunks in slot order (batch, lex).  A
@@ -101,12 +101,19 @@ __global__ void __launch_bounds__(256, GHOST_MINB) ghost_persistent_kernel(Ghost
     if (gtrace) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tg0));
     if (node >= 0) {
       const int64_t base = a.base[s];
-      double x[M], y[M];
+      // the row weights go to shared memory by cp.async (in flight during the
+      // wait, no registers held); the block values stay in registers
+      extern __shared__ double wsm[];  // [M][blockDim.x]
 #pragma unroll
       for (int j = 0; j < M; ++j) {
-        x[j] = __ldg(a.w + (int64_t)j * a.ng + s);
-        y[j] = __ldcg(u + base + block_offset<D>(a.g, j));
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&wsm[j * blockDim.x + threadIdx.x]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(a.w + (int64_t)j * a.ng + s)
+                     : "memory");
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      double y[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) y[j] = __ldcg(u + base + block_offset<D>(a.g, j));
       const double gv = a.gval[s], dt = a.dtau[s], uo = __ldcg(u + node);
       const uint32_t vm = vmask[s];
       const int k0 = dep_off[s];
@@ -142,6 +149,10 @@ __global__ void __launch_bounds__(256, GHOST_MINB) ghost_persistent_kernel(Ghost
         for (int k = kw + WMAX; k < d1; ++k) wait_pair(pair + 2 * (int64_t)dep[k], backoff);
       }
       if (gtrace) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tg1));
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      double x[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) x[j] = wsm[j * blockDim.x + threadIdx.x];
       const double dot = blas_ddot<M>(x, y);
       const double nv = uo + dt * (gv - dot);
       if (!defer) __stcg(u + node, nv);  // defer: u keeps the old value until the write-back
@@ -226,12 +237,20 @@ void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_o
   const int64_t warps = a.ng / 32;
   int blocks = (int)std::min<int64_t>((warps + 7) / 8, (int64_t)sms * blocks_per_sm);
   if (blocks < 1) blocks = 1;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ghost_persistent_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(27 * 256 * sizeof(double)));
+    cudaFuncSetAttribute(ghost_persistent_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(9 * 256 * sizeof(double)));
+    attr = true;
+  }
   if (a.g.d == 3)
-    ghost_persistent_kernel<3><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace,
-                                                       defer);
+    ghost_persistent_kernel<3><<<blocks, 256, 27 * 256 * sizeof(double), st>>>(a, u, dep_off, dep, vmask, pair, cursor,
+                                                                               backoff, gtrace, defer);
   else
-    ghost_persistent_kernel<2><<<blocks, 256, 0, st>>>(a, u, dep_off, dep, vmask, pair, cursor, backoff, gtrace,
-                                                       defer);
+    ghost_persistent_kernel<2><<<blocks, 256, 9 * 256 * sizeof(double), st>>>(a, u, dep_off, dep, vmask, pair, cursor,
+                                                                              backoff, gtrace, defer);
 }
 
 
