@@ -315,37 +315,35 @@ void launch_residual_interior(const Geom& g, const uint8_t* labels, const double
                               const double* f, double* r, unsigned long long* maxbits,
                               cudaStream_t st) {
   if (g.d == 3 && !getenv("GMG_RES_ROWS")) {
-    // tile 8 rows x 64 columns, 5-slot ring (4 CTAs per SM); GMG_RES_TILE=16: 16 rows, 2 CTAs per SM (on par)
-    static int tj_sel = -1;
-    if (tj_sel < 0) {
-      const char* e = getenv("GMG_RES_TILE");
-      tj_sel = e ? atoi(e) : 8;
+    // 8-row x 64-column tiles; ring of 4 plane slots (5 CTAs per SM) on the
+    // largest grids, 5 slots (4 CTAs per SM) below N = 512 (measured per level)
+    static bool attr = false;
+    if (!attr) {
       cudaFuncSetAttribute(residual_march3_kernel<true, 8, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(ResMarchSmem<8, 5>));
       cudaFuncSetAttribute(residual_march3_kernel<false, 8, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(ResMarchSmem<8, 5>));
-      cudaFuncSetAttribute(residual_march3_kernel<true, 16, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(ResMarchSmem<16, 5>));
-      cudaFuncSetAttribute(residual_march3_kernel<false, 16, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(ResMarchSmem<16, 5>));
+      cudaFuncSetAttribute(residual_march3_kernel<true, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ResMarchSmem<8, 4>));
+      cudaFuncSetAttribute(residual_march3_kernel<false, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ResMarchSmem<8, 4>));
+      attr = true;
     }
-    const int TJ = tj_sel == 8 ? 8 : 16;
-    const int per_sm = TJ == 8 ? 4 : 2;
-    const int64_t tk = (g.N - 1 + RM_TK - 1) / RM_TK, tj = (g.N - 1 + TJ - 1) / TJ;
+    const bool big = g.N >= 512;
+    const int per_sm = big ? 5 : 4;
+    const int64_t tk = (g.N - 1 + RM_TK - 1) / RM_TK, tj = (g.N - 1 + 8 - 1) / 8;
     const int64_t segs = std::max<int64_t>(1, std::min<int64_t>((g.N - 1) / 4, 148 * per_sm / (tk * tj)));
     dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)segs);
-    if (TJ == 8) {
+    if (big) {
       if (r)
-        residual_march3_kernel<true, 8, 5><<<grid, 8 * 32, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits);
+        residual_march3_kernel<true, 8, 4><<<grid, 256, sizeof(ResMarchSmem<8, 4>), st>>>(g, labels, u, f, r, maxbits);
       else
-        residual_march3_kernel<false, 8, 5><<<grid, 8 * 32, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits);
+        residual_march3_kernel<false, 8, 4><<<grid, 256, sizeof(ResMarchSmem<8, 4>), st>>>(g, labels, u, f, r, maxbits);
     } else {
       if (r)
-        residual_march3_kernel<true, 16, 5><<<grid, 16 * 32, sizeof(ResMarchSmem<16, 5>), st>>>(g, labels, u, f, r,
-                                                                                               maxbits);
+        residual_march3_kernel<true, 8, 5><<<grid, 256, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits);
       else
-        residual_march3_kernel<false, 16, 5><<<grid, 16 * 32, sizeof(ResMarchSmem<16, 5>), st>>>(g, labels, u, f, r,
-                                                                                                maxbits);
+        residual_march3_kernel<false, 8, 5><<<grid, 256, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits);
     }
   } else if (g.d == 3 && getenv("GMG_RES_STREAM")) {
     dim3 grid((unsigned)((g.N - 1 + RT_K - 1) / RT_K), (unsigned)((g.N - 1 + RT_J - 1) / RT_J));
