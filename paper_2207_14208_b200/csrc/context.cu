@@ -157,6 +157,8 @@ struct gmg_ctx {
   bool gs_trace = false;       // record the GS task timeline (GMG_GS_TRACE=1)
   bool gs_ws = false;          // use the older TMA-ring GS kernel (GMG_GS_WS=1)
   int gs_variant = 0;          // GS implementation variant (GMG_GS_VARIANT, experiments)
+  int64_t band_coop_max = 200000;  // band extensions up to this many nodes: one cooperative launch (GMG_BAND_COOP;
+                                   // 128^3 49 -> 40 us, 64^3 47 -> 30 us; 256^3 (533 k nodes) was slower)
   int halo_multi = -1;         // GS halo loader: -1 by level size, 0 two-batch, 1 multi-batch (GMG_GS_HALO)
   int ghost_bps = 8;           // ghost sweep: CTAs per SM (GMG_GHOST_BPS)
   bool ghost_raw_only = true;  // ghost sweep: new values only in the pairs until a write-back launch, so
@@ -572,6 +574,12 @@ int op_extend(gmg_ctx* ctx, DevLevel& l, double* x) {
   if (l.nb == 0) return 0;
   Scope s(ctx, 3);
   BandArgs a = band_args(l);
+  // small bands: one cooperative launch for all phases
+  if (l.nb <= ctx->band_coop_max &&
+      launch_band_coop(a, x, l.bfs_off.data(), (int)l.bfs_off.size() - 1, ctx->stream)) {
+    ctx->launches++;
+    return 0;
+  }
   for (size_t gi = 0; gi + 1 < l.bfs_off.size(); ++gi) {
     launch_band_bfs(a, x, l.bfs_off[gi], l.bfs_off[gi + 1], ctx->stream);
     ctx->launches++;
@@ -932,6 +940,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_WS")) ctx->gs_ws = e[0] == '1';
   if (const char* e = getenv("GMG_GS_VARIANT")) ctx->gs_variant = atoi(e);
   if (const char* e = getenv("GMG_GS_HALO")) ctx->halo_multi = atoi(e);
+  if (const char* e = getenv("GMG_BAND_COOP")) ctx->band_coop_max = atoll(e);
   if (const char* e = getenv("GMG_GHOST_BPS")) ctx->ghost_bps = std::max(1, atoi(e));
   if (const char* e = getenv("GMG_GHOST_RAW")) ctx->ghost_raw_only = e[0] != '0';
   if (const char* e = getenv("GMG_GHOST_LEVELS")) ctx->ghost_levels = e[0] == '1';

@@ -84,6 +84,7 @@ void launch_residual_interior(const Geom& g, const uint8_t* labels, const double
                               cudaStream_t st);
 void launch_band_bfs(const BandArgs& a, double* x, int64_t lo, int64_t hi, cudaStream_t st);
 void launch_band_transport(const BandArgs& a, double* x, cudaStream_t st);
+bool launch_band_coop(const BandArgs& a, double* x, const int64_t* goff, int ngroups, cudaStream_t st);
 void launch_restrict_interior(const Geom& gf, const double* r_f, const Geom& gc, const uint32_t* rmask,
                               double* f_c, cudaStream_t st);
 void launch_res_restrict3(const Geom& gf, const uint8_t* labels, const double* u, const double* f, const Geom& gc,

@@ -8,7 +8,11 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "gmg_kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gmg {
 
@@ -1000,6 +1004,78 @@ void launch_band_transport(const BandArgs& a, double* x, cudaStream_t st) {
       band_iter_kernel<2><<<blocks, 256, 0, st>>>(a, vin, vout);
   }
   band_scatter_kernel<<<blocks, 256, 0, st>>>(a, a.v0, x);  // six steps: result back in v0
+}
+
+// The whole band extension of a small level in one cooperative launch: the
+// BFS groups, the gather, the six Jacobi steps and the scatter as phases of a
+// grid-stride loop separated by grid-wide barriers -- the same per-node
+// arithmetic as band_bfs_kernel / band_*_kernel, without ~11 launches.
+template <int D>
+__global__ void __launch_bounds__(256) band_coop_kernel(BandArgs a, double* __restrict__ x, int64_t g1, int64_t g2,
+                                                        int64_t g3) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, ts = (int64_t)gridDim.x * blockDim.x;
+  const int64_t s[3] = {a.g.s0, a.g.s1, a.g.s2};
+  const int64_t goff[4] = {0, g1, g2, g3};
+  for (int gi = 0; gi < 3; ++gi) {
+    if (goff[gi + 1] <= goff[gi]) continue;
+    for (int64_t q = goff[gi] + t0; q < goff[gi + 1]; q += ts) {
+      const int64_t i = a.idx[q];
+      const unsigned mk = a.mask[q];
+      double t[2 * D];
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const bool bit = (mk >> (2 * k + j)) & 1u;
+          t[2 * k + j] = bit ? x[j ? i + s[k] : i - s[k]] * 1.0 : 0.0;
+        }
+      x[i] = seq_sum<2 * D>(t) / (double)__popc(mk);
+    }
+    grid.sync();
+  }
+  for (int64_t q = t0; q < a.nb + a.nfix; q += ts) {
+    const double v = q < a.nb ? x[a.idx[q]] : x[a.fixpos[q - a.nb]];
+    a.v0[q] = v;
+    if (q >= a.nb) a.v1[q] = v;
+  }
+  grid.sync();
+  for (int it = 0; it < 6; ++it) {
+    const double* vin = (it & 1) ? a.v1 : a.v0;
+    double* vout = (it & 1) ? a.v0 : a.v1;
+    for (int64_t q = t0; q < a.nb; q += ts) {
+      const double vi = vin[q];
+      double t[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) t[k] = a.absn[q * D + k] * (vi - vin[a.nbr[q * D + k]]);
+      vout[q] = vi - 0.5 * seq_sum<D>(t);
+    }
+    grid.sync();
+  }
+  for (int64_t q = t0; q < a.nb; q += ts) x[a.idx[q]] = a.v0[q];
+}
+
+// returns false when the cooperative launch is not possible (caller falls back)
+bool launch_band_coop(const BandArgs& a, double* x, const int64_t* goff, int ngroups, cudaStream_t st) {
+  if (ngroups > 3) return false;
+  int64_t g[3] = {0, 0, 0};
+  for (int k = 0; k < 3; ++k) g[k] = goff[std::min(k + 1, ngroups)];
+  static int occ[2] = {0, 0};
+  int& o = occ[a.g.d == 3 ? 1 : 0];
+  if (o == 0) {
+    if (a.g.d == 3)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, band_coop_kernel<3>, 256, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, band_coop_kernel<2>, 256, 0);
+    if (o < 1) o = 1;
+  }
+  const int64_t want = (a.nb + a.nfix + 255) / 256;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, 148 * (int64_t)std::min(o, 2)));
+  BandArgs aa = a;
+  void* args[] = {&aa, &x, &g[0], &g[1], &g[2]};
+  cudaError_t e = a.g.d == 3 ? cudaLaunchCooperativeKernel((void*)band_coop_kernel<3>, blocks, 256, args, 0, st)
+                             : cudaLaunchCooperativeKernel((void*)band_coop_kernel<2>, blocks, 256, args, 0, st);
+  return e == cudaSuccess;
 }
 
 __global__ void abs_max_kernel(const double* __restrict__ u, int64_t n, unsigned long long* maxbits) {
