@@ -102,7 +102,7 @@ class ClockSampler:
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4}
 
-    def __init__(self, index, period=0.25):
+    def __init__(self, index, period=0.02):
         self.index = index
         self.period = period
         self.samples = []
