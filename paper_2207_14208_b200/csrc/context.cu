@@ -58,6 +58,8 @@ struct DevLevel {
   int64_t *gnode = nullptr, *gbase = nullptr;
   double *gw = nullptr, *gdtau = nullptr, *gval = nullptr, *gtmp = nullptr;
   uint8_t* gprom = nullptr;
+  double* gwl = nullptr;                           // ghost weights in lexicographic order [m][ng]
+  int64_t *gbasel = nullptr, *gnodel = nullptr;    // block base / node, lexicographic order
   int32_t *slot2lex = nullptr, *lex2slot = nullptr;
   std::vector<int64_t> batch_off;  // slot offsets of sweep batches
   // band
@@ -254,7 +256,7 @@ void free_level(DevLevel& l) {
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
                   l.bscratch, l.tasks, l.tempty, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
                   l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off,
-                  l.bfixpos, l.bnbr, l.bv0, l.bv1, l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g,
+                  l.bfixpos, l.bnbr, l.bv0, l.bv1, l.gwl, l.gbasel, l.gnodel, l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g,
                   l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part, l.nd_crow, l.nd_ccol, l.nd_cval};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -565,7 +567,11 @@ int op_res_int(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
 int op_res_ghost(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
   if (l.ng == 0) return 0;
   Scope s(ctx, slot ? 7 : 2);
-  launch_residual_ghost(ghost_args(l), l.u, slot ? nullptr : l.rE, slot, ctx->stream);
+  if (l.gwl)
+    launch_residual_ghost_lex(ghost_args(l), l.gwl, l.gbasel, l.gnodel, l.lex2slot, l.ng, l.u, slot ? nullptr : l.rE,
+                              slot, ctx->stream);
+  else
+    launch_residual_ghost(ghost_args(l), l.u, slot ? nullptr : l.rE, slot, ctx->stream);
   ctx->launches++;
   return 0;
 }
@@ -1125,6 +1131,21 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
         upload(ctx, &l.dbatch_off, l.batch_off.data(), maxb + 2))
       return -1;
     GMG_CHECK(ctx, cudaMemset(l.gval, 0, sizeof(double) * ns));
+    // the same rows in lexicographic order: the ghost residual walks them
+    // spatially (neighbouring ghosts share their 3^d blocks' sectors)
+    {
+      std::vector<int64_t> nodel((size_t)ng), basel((size_t)ng);
+      std::vector<double> wl((size_t)m * ng);
+      for (int64_t i = 0; i < ng; ++i) {
+        const int64_t sl = l2s[i];
+        nodel[i] = node[sl];
+        basel[i] = base[sl];
+        for (int j = 0; j < m; ++j) wl[(size_t)j * ng + i] = w[(size_t)j * ns + sl];
+      }
+      if (upload(ctx, &l.gnodel, nodel.data(), ng) || upload(ctx, &l.gbasel, basel.data(), ng) ||
+          upload(ctx, &l.gwl, wl.data(), (int64_t)m * ng))
+        return -1;
+    }
   } else {
     l.batch_off.assign(1, 0);
     l.nslots = 0;

@@ -324,6 +324,42 @@ void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,
     residual_ghost_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(a, u, r_ext, maxbits);
 }
 
+// Same residual over the ghosts in lexicographic order (weights, bases and
+// nodes stored in that order; the right-hand side stays in slot order).
+template <int D>
+__global__ void __launch_bounds__(256) residual_ghost_lex_kernel(GhostArgs a, const double* __restrict__ wl,
+                                                                 const int64_t* __restrict__ basel,
+                                                                 const int64_t* __restrict__ nodel,
+                                                                 const int32_t* __restrict__ l2s, int64_t ng,
+                                                                 const double* __restrict__ u,
+                                                                 double* __restrict__ r_ext,
+                                                                 unsigned long long* maxbits) {
+  constexpr int M = D == 3 ? 27 : 9;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double am = 0.0;
+  if (i < ng) {
+    const int64_t base = basel[i];
+    double p[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) p[j] = __ldg(wl + (int64_t)j * ng + i) * u[base + block_offset<D>(a.g, j)];
+    const double r = a.gval[l2s[i]] - np_sum<M>(p);
+    if (r_ext) r_ext[nodel[i]] = r;
+    am = fabs(r);
+  }
+  block_max_commit(am, maxbits);
+}
+
+void launch_residual_ghost_lex(const GhostArgs& a, const double* wl, const int64_t* basel, const int64_t* nodel,
+                               const int32_t* l2s, int64_t ng, const double* u, double* r_ext,
+                               unsigned long long* maxbits, cudaStream_t st) {
+  if (ng == 0) return;
+  const int64_t blocks = (ng + 255) / 256;
+  if (a.g.d == 3)
+    residual_ghost_lex_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(a, wl, basel, nodel, l2s, ng, u, r_ext, maxbits);
+  else
+    residual_ghost_lex_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(a, wl, basel, nodel, l2s, ng, u, r_ext, maxbits);
+}
+
 // Full-weighting row entry e of a 3^D block, ((1*a)*b)*c.
 template <int D>
 __device__ __forceinline__ double fw_entry(int e) {

@@ -79,6 +79,9 @@ void launch_ghost_persistent(const GhostArgs& a, double* u, const int32_t* dep_o
 void launch_ghost_writeback(const GhostArgs& a, const double* pair, double* u, cudaStream_t st);
 void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,
                            unsigned long long* maxbits, cudaStream_t st);
+void launch_residual_ghost_lex(const GhostArgs& a, const double* wl, const int64_t* basel, const int64_t* nodel,
+                               const int32_t* l2s, int64_t ng, const double* u, double* r_ext,
+                               unsigned long long* maxbits, cudaStream_t st);
 void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,
                               const double* f, double* r, unsigned long long* maxbits,
                               cudaStream_t st);
