@@ -614,7 +614,7 @@ int op_res_restrict(gmg_ctx* ctx, DevLevel& f, DevLevel& c) {
 int op_restrict_ghost(gmg_ctx* ctx, DevLevel& f, DevLevel& c) {
   if (c.ng == 0) return 0;
   Scope s(ctx, 4);
-  launch_restrict_ghost(f.g, f.labels, f.rE, ghost_args(c), c.gval, ctx->stream);
+  launch_restrict_ghost(f.g, f.labels, f.rE, ghost_args(c), c.gval, c.lex2slot, c.ng, ctx->stream);
   ctx->launches++;
   return 0;
 }

@@ -383,10 +383,14 @@ __device__ __forceinline__ double fw_entry(int e) {
 template <int D>
 __global__ void __launch_bounds__(256) restrict_ghost_kernel(Geom gf, const uint8_t* __restrict__ lab_f,
                                                              const double* __restrict__ r_ext,
-                                                             GhostArgs c, double* __restrict__ gval_c) {
+                                                             GhostArgs c, double* __restrict__ gval_c,
+                                                             const int32_t* __restrict__ order, int64_t n) {
+  // order: coarse ghosts visited in lexicographic order (slot = order[t]),
+  // so neighbouring threads read neighbouring fine blocks; else slot order
   constexpr int M = D == 3 ? 27 : 9;
-  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s >= c.ng) return;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t s = order ? order[t] : t;
   if (c.promoted[s] || c.node[s] < 0) {
     gval_c[s] = 0.0;
     return;
@@ -428,14 +432,17 @@ __global__ void __launch_bounds__(256) restrict_ghost_kernel(Geom gf, const uint
 }
 
 void launch_restrict_ghost(const Geom& gf, const uint8_t* lab_f, const double* r_ext,
-                           const GhostArgs& coarse, double* gval_c, cudaStream_t st) {
+                           const GhostArgs& coarse, double* gval_c, const int32_t* order, int64_t n_lex,
+                           cudaStream_t st) {
   if (coarse.ng == 0) return;
   const int threads = 256;
-  const int64_t blocks = (coarse.ng + threads - 1) / threads;
+  const int64_t n = order ? n_lex : coarse.ng;
+  const int64_t blocks = (n + threads - 1) / threads;
+  if (n == 0) return;
   if (gf.d == 3)
-    restrict_ghost_kernel<3><<<(unsigned)blocks, threads, 0, st>>>(gf, lab_f, r_ext, coarse, gval_c);
+    restrict_ghost_kernel<3><<<(unsigned)blocks, threads, 0, st>>>(gf, lab_f, r_ext, coarse, gval_c, order, n);
   else
-    restrict_ghost_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(gf, lab_f, r_ext, coarse, gval_c);
+    restrict_ghost_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(gf, lab_f, r_ext, coarse, gval_c, order, n);
 }
 
 }  // namespace gmg

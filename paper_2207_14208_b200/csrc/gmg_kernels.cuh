@@ -95,7 +95,8 @@ void launch_res_restrict3(const Geom& gf, const uint8_t* labels, const double* u
 void launch_restrict_mask(const Geom& gf, const uint8_t* lab_f, const Geom& gc, const uint8_t* lab_c,
                           uint32_t* rmask, cudaStream_t st);
 void launch_restrict_ghost(const Geom& gf, const uint8_t* lab_f, const double* r_ext,
-                           const GhostArgs& coarse, double* gval_c, cudaStream_t st);
+                           const GhostArgs& coarse, double* gval_c, const int32_t* order, int64_t n_lex,
+                           cudaStream_t st);
 void launch_interp_add(const Geom& gf, const uint8_t* lab_f, double* u_f, const Geom& gc,
                        const double* e_c, cudaStream_t st);
 void launch_abs_max(const double* u, int64_t n, unsigned long long* maxbits, cudaStream_t st);
