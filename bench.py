@@ -323,7 +323,13 @@ def run_b200(args, rank, world, local_rank):
         d2h = 8 * p0.n_nodes + 16 * (args.steps + 1)
         e2e = {"value": dof * args.steps * world / dt, "unit": "DOF*cycles/s",
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-               "solve_s": dt, "cycles": args.steps, "final_residual": rep.residual_norms[-1]}
+               "solve_s": dt, "cycles": args.steps, "final_residual": rep.residual_norms[-1],
+               # convergence factor of this solve: geometric mean of the per-cycle
+               # residual ratios after the first cycle (the reference's rho is the
+               # mean ratio over cycles 11-15 of a 16-cycle measure_rho run)
+               "conv_factor": (rep.residual_norms[-1] / rep.residual_norms[1]) ** (1.0 / (len(rep.residual_norms) - 2))
+               if len(rep.residual_norms) > 2 and rep.residual_norms[1] > 0 else None,
+               "rho_sequence": [float(x) for x in rep.rho_sequence]}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
