@@ -159,6 +159,15 @@ int gmg_synchronize(gmg_ctx *ctx);
 
 /* Kernels launched by this context so far. */
 int64_t gmg_launch_count(const gmg_ctx *ctx);
+/* Batched solves (many contexts, one stream each; inf norm): norm_begin
+ * enqueues residual_norm's two maxima (ref solver.py:135-142) and max|u|
+ * (the renormalisation guard, solver.py:239-243) of the finest level with an
+ * asynchronous copy; norm_end waits for this context's stream and returns
+ * {max|r_int|, max|r_g|, max|u|}; scale_u multiplies the finest u. */
+int gmg_norm_begin(gmg_ctx *ctx);
+int gmg_norm_end(gmg_ctx *ctx, double *out3);
+int gmg_scale_u(gmg_ctx *ctx, double factor);
+
 /* Diagnostics: with GMG_GS_TRACE=1 in the environment the Gauss-Seidel
  * kernel records 16 int64 per task (start/end globaltimer ns, SM id, compute
  * warp cycles waiting for data / in total, loader waits and idle polls, see

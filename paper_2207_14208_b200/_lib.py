@@ -53,6 +53,9 @@ SIGNATURES = {
     "gmg_cycle": (_i, [_p, _i]),
     "gmg_residual_norm": (_i, [_p, _i, _p]),
     "gmg_abs_max_scale": (_i, [_p, _d, _d, _p, _p]),
+    "gmg_norm_begin": (_i, [_p]),
+    "gmg_norm_end": (_i, [_p, _p]),
+    "gmg_scale_u": (_i, [_p, _d]),
     "gmg_synchronize": (_i, [_p]),
     "gmg_launch_count": (_i64, [_p]),
     "gmg_debug_gs_trace": (_i64, [_p, _i, _p, _i64]),
@@ -239,6 +242,17 @@ class Context:
         scaled = np.zeros(1, dtype=np.int32)
         self.check(self.lib.gmg_abs_max_scale(self.ctx, threshold, factor, ptr(peak), ptr(scaled)))
         return float(peak[0]), bool(scaled[0])
+
+    def norm_begin(self):
+        self.check(self.lib.gmg_norm_begin(self.ctx))
+
+    def norm_end(self):
+        out = np.zeros(3)
+        self.check(self.lib.gmg_norm_end(self.ctx, ptr(out)))
+        return float(out[0]), float(out[1]), float(out[2])
+
+    def scale_u(self, factor):
+        self.check(self.lib.gmg_scale_u(self.ctx, factor))
 
     def synchronize(self):
         self.check(self.lib.gmg_synchronize(self.ctx))

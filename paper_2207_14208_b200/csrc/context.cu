@@ -1680,6 +1680,42 @@ int gmg_residual_norm(gmg_ctx* ctx, int li, double* out) {
   return 0;
 }
 
+// Asynchronous form of residual_norm + the renormalisation check for batched
+// solves (many contexts, one stream each): begin enqueues the inf-norm parts
+// and max|u| of the finest level with a D2H copy into pinned memory; end waits
+// for this context's stream only.
+int gmg_norm_begin(gmg_ctx* ctx) {
+  if (ctx->norm != 0) return fail(ctx, "batched norms are inf-norms");
+  if (!ctx->L[0].ready) return fail(ctx, "level not set");
+  cudaSetDevice(ctx->device);
+  DevLevel& l = ctx->L[0];
+  ctx->cur_level = 0;
+  GMG_CHECK(ctx, cudaMemsetAsync(ctx->dmax, 0, 3 * sizeof(unsigned long long), ctx->stream));
+  if (op_res_ghost(ctx, l, ctx->dmax + 1) || op_res_int(ctx, l, ctx->dmax)) return -1;
+  launch_abs_max(l.u, l.g.nodes, ctx->dmax + 2, ctx->stream);
+  ctx->launches++;
+  GMG_CHECK(ctx, cudaMemcpyAsync(ctx->hmax, ctx->dmax, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  return 0;
+}
+
+int gmg_norm_end(gmg_ctx* ctx, double* out3) {
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  GMG_CHECK(ctx, cudaGetLastError());
+  if (ctx->prof) profile_flush(ctx);
+  std::memcpy(out3, ctx->hmax, 3 * sizeof(double));
+  return 0;
+}
+
+int gmg_scale_u(gmg_ctx* ctx, double factor) {
+  cudaSetDevice(ctx->device);
+  DevLevel& l = ctx->L[0];
+  launch_scale(l.u, l.g.nodes, factor, ctx->stream);
+  ctx->launches++;
+  GMG_CHECK(ctx, cudaGetLastError());
+  return 0;
+}
+
 int gmg_abs_max_scale(gmg_ctx* ctx, double threshold, double factor, double* peak, int* scaled) {
   cudaSetDevice(ctx->device);
   DevLevel& l = ctx->L[0];

@@ -40,7 +40,8 @@ from .plan import coarsest_system
 from .smoothing import SmootherConfig
 from .transfer import build_hierarchy
 
-__all__ = ["MultigridSolver", "build_solver", "measure_rho", "CycleConfig", "CycleReport"]
+__all__ = ["MultigridSolver", "build_solver", "measure_rho", "solve_batched", "measure_rho_batched", "CycleConfig",
+           "CycleReport"]
 
 
 COARSE_BACKENDS = ("superlu", "device-inverse")
@@ -317,6 +318,100 @@ class MultigridSolver(CycleDriver):
 
     def _abs_max_scale(self):
         return self.ctx.abs_max_scale(1e-250, 1e250)
+
+
+def solve_batched(solvers, us=None, cycles=None, seed=42):
+    """``[s.solve(u, cycles, seed=seed) for s in solvers]`` with the solvers'
+    cycles interleaved: every round enqueues one cycle and the asynchronous
+    residual norm / max|u| on each solver's own stream, then collects them, so
+    many small problems (the BLFA parameter sweeps of the paper, reference
+    cli.py:154-194) keep the GPU busy together instead of one after the other.
+    Same control flow per solver as CycleDriver.solve (reference
+    solver.py:215-269) and bitwise the same results; inf norm only."""
+    from .cycle import DIVERGENCE_FACTOR, MIN_CYCLES_FOR_RHO, RHO_WINDOW
+
+    n = len(solvers)
+    us = [None] * n if us is None else list(us)
+    cyc = [s.cycle_cfg.cycles if cycles is None else cycles for s in solvers]
+    for s in solvers:
+        if s.cycle_cfg.norm == NORM_L2:
+            raise NotImplementedError("solve_batched uses the inf norm")
+    st = []
+    for i, s in enumerate(solvers):
+        u = s.initial_field(seed) if us[i] is None else us[i]
+        us[i] = u
+        s._set_data(s.f_fine, s.g_fine)
+        s._put_u(np.ascontiguousarray(u, dtype=np.float64))
+        st.append({"ln": [], "scale": 0.0, "div": False, "ran": 0, "active": True, "pending": False})
+
+    def norm_of(s, parts):
+        m_int, m_g, peak = parts
+        p = s.plans[0]
+        m = m_int if p.n_internal else 0.0
+        if p.n_ghosts:
+            m = max(m, m_g)
+        return m, peak
+
+    for s in solvers:
+        s.ctx.norm_begin()
+    for s, t in zip(solvers, st):
+        m, _ = norm_of(s, s.ctx.norm_end())
+        t["ln"].append((math.log(m) if m > 0.0 else -math.inf) + t["scale"])
+    for m_ in range(max(cyc) if cyc else 0):
+        live = [i for i in range(n) if st[i]["active"] and m_ < cyc[i]]
+        if not live:
+            break
+        for i in live:
+            s, t = solvers[i], st[i]
+            if t["pending"]:
+                s.ctx.scale_u(1e250)
+                t["pending"] = False
+            s.ctx.cycle(1)
+            s.ctx.norm_begin()
+        for i in live:
+            s, t = solvers[i], st[i]
+            r, peak = norm_of(s, s.ctx.norm_end())
+            t["ln"].append((math.log(r) if r > 0.0 else -math.inf) + t["scale"])
+            t["ran"] = m_ + 1
+            if t["ln"][-1] - t["ln"][0] > math.log(DIVERGENCE_FACTOR):
+                t["div"] = True
+                t["active"] = False
+                continue
+            if 0.0 < peak < 1e-250:  # CycleDriver._abs_max_scale
+                t["pending"] = True
+                t["scale"] -= math.log(1e250)
+    out = []
+    for i, (s, t) in enumerate(zip(solvers, st)):
+        if t["pending"]:
+            s.ctx.scale_u(1e250)
+        u = s._fetch_u(us[i])
+        ln = t["ln"]
+        norms = [math.exp(v) if v > -math.inf else 0.0 for v in ln]
+        rho_seq = [math.exp(ln[k + 1] - ln[k]) if ln[k] > -math.inf else 0.0 for k in range(len(ln) - 1)]
+        lo, hi = RHO_WINDOW
+        rho = 1.0 if t["div"] else (float(np.mean(rho_seq[lo:hi + 1])) if t["ran"] >= MIN_CYCLES_FOR_RHO else None)
+        out.append((u, CycleReport(residual_norms=norms, rho_sequence=rho_seq, rho_asymptotic=rho,
+                                   diverged=t["div"], cycles_run=t["ran"], scheme=s.cycle_cfg.scheme,
+                                   n_levels=s.n_levels, norm=s.cycle_cfg.norm, seed=seed)))
+    return out
+
+
+def measure_rho_batched(solvers, seed=42, cycles=16):
+    """measure_rho (reference solver.py:282-298) for many solvers at once."""
+    from .cycle import MIN_CYCLES_FOR_RHO
+
+    cycles = max(cycles, MIN_CYCLES_FOR_RHO)
+    saved = [(s.f_fine, s.g_fine, s.eliminated_values) for s in solvers]
+    for s in solvers:
+        s.f_fine = np.zeros_like(s.f_fine)
+        s.g_fine = np.zeros_like(s.g_fine)
+        s.eliminated_values = np.zeros_like(s.eliminated_values)
+    try:
+        res = solve_batched(solvers, cycles=cycles, seed=seed)
+    finally:
+        for s, (f, g, e) in zip(solvers, saved):
+            s.f_fine, s.g_fine, s.eliminated_values = f, g, e
+    return [r for _, r in res]
 
 
 def build_solver(grid, phi, spec, eliminated_faces=(), smoother=None, cycle=None,

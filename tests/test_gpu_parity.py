@@ -209,3 +209,29 @@ def test_l2_norm_3d_matches_oracle(gpu_available):
     _, rd = dev.solve(u=u0.copy())
     _, ro = ref.solve(u=u0.copy())
     assert rd.residual_norms == ro.residual_norms
+
+
+def test_batched_solves_match_individual(gpu_available):
+    """solve_batched / measure_rho_batched (interleaved solvers on their own
+    streams) give bitwise the results of one-at-a-time solves."""
+    from paper_2207_14208_b200 import configs as CF
+    from paper_2207_14208_b200.cycle import CycleDriver
+    from paper_2207_14208_b200.solver import measure_rho_batched, solve_batched
+    from paper_2207_14208_b200.transfer import build_hierarchy
+
+    def make(setup):
+        levels = build_hierarchy(setup.grid, setup.phi, setup.faces, coarsest_min=setup.coarsest_min)
+        plans, f, g, e = CycleDriver.problem_data(levels, setup.spec, setup.smoother, setup.default_variant)
+        return plans, MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle,
+                                                 coarse_backend="device-inverse")
+
+    setups = [CF.config_disk(64, cycles=12), CF.config_ball(32, cycles=10), CF.config_disk(128, cycles=12)]
+    solvers = [make(s)[1] for s in setups]
+    want = [s.solve(u=np.zeros(s.plans[0].n_nodes))for s in solvers]
+    got = solve_batched(solvers, us=[np.zeros(s.plans[0].n_nodes) for s in solvers])
+    for (uw, rw), (ug, rg) in zip(want, got):
+        assert rg.residual_norms == rw.residual_norms
+        assert np.array_equal(ug.view(np.uint64), uw.view(np.uint64))
+    rho_want = [measure_rho(s, seed=42).residual_norms for s in solvers]
+    rho_got = [r.residual_norms for r in measure_rho_batched(solvers, seed=42)]
+    assert rho_got == rho_want
