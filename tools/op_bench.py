@@ -52,6 +52,8 @@ for i, p in enumerate(plans[:-1]):
     for nm, op, kc in OPS:
         if nm == "extend_u" and i == 0:
             continue
+        if nm == "res_restrict" and plans[i].d != 3:
+            continue
         lvl = i + 1 if nm == "extend_u" else i
         ctx.apply(lvl, op)
         ctx.synchronize()
