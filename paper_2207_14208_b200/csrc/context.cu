@@ -169,6 +169,8 @@ struct gmg_ctx {
   int ghost_backoff = 300;     // ghost sweep: poll back-off ns (GMG_GHOST_BACKOFF)
   int gs_sleep[4] = {500, 500, 20, 200};  // GS loader / writer back-off (ns), GMG_GS_SLEEP=u,f,h,w  // one launch per ghost batch instead of the persistent sweep
   int ws_ctas_per_sm = 4;
+  int gs_macro = 1;            // 3-D GS: two line chains per lane (gs_macro.cu; GMG_GS_MACRO=0: gs_diag.cu)
+  int macro_ctas = 0;          // its resident CTAs per SM (occupancy query on first use)
   bool prof = false;
   int prof_mask = 0;   // bit k: time kernel class k
   int cur_level = -1;  // level tag for profiling records
@@ -501,7 +503,10 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
     a.trace = l.trace;
   }
   if (ctx->gs_max_tasks > 0) a.ntasks = std::min(a.ntasks, ctx->gs_max_tasks);  // timing experiments only
-  if (l.diag_gs)
+  if (l.diag_gs && l.g.d == 3 && ctx->gs_macro) {
+    if (ctx->macro_ctas <= 0) ctx->macro_ctas = gs_macro_ctas_per_sm();
+    launch_gs_macro(a, l.maps, std::min(a.ntasks, ctx->macro_ctas * ctx->sms), ctx->stream);
+  } else if (l.diag_gs)
     launch_gs_diag(a, l.maps, std::min(a.ntasks, ctx->ws_ctas_per_sm * ctx->sms), ctx->stream);
   else if (l.ws_gs)
     launch_gs_ws(a, l.maps, std::min(a.ntasks, ctx->ws_ctas_per_sm * ctx->sms), ctx->stream);
@@ -946,6 +951,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_WS")) ctx->gs_ws = e[0] == '1';
   if (const char* e = getenv("GMG_GS_VARIANT")) ctx->gs_variant = atoi(e);
   if (const char* e = getenv("GMG_GS_HALO")) ctx->halo_multi = atoi(e);
+  if (const char* e = getenv("GMG_GS_MACRO")) ctx->gs_macro = atoi(e);
   if (const char* e = getenv("GMG_BAND_COOP")) ctx->band_coop_max = atoll(e);
   if (const char* e = getenv("GMG_GHOST_BPS")) ctx->ghost_bps = std::max(1, atoi(e));
   if (const char* e = getenv("GMG_GHOST_RAW")) ctx->ghost_raw_only = e[0] != '0';

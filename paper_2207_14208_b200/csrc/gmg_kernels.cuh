@@ -67,6 +67,8 @@ void launch_gs_ws(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st
 size_t gs_ws_smem();
 void launch_gs_diag(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st);
 size_t gs_diag_smem();
+void launch_gs_macro(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st);
+int gs_macro_ctas_per_sm();
 void configure_gs_kernels();  // set max dynamic shared memory of the GS / GEMV kernels
 
 void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, double* pair, cudaStream_t st);

@@ -251,6 +251,7 @@ size_t gs_stream_smem_per_warp() { return sizeof(WarpRing); }
 
 void configure_gs_ws();
 void configure_gs_diag();
+void configure_gs_macro();
 void configure_dense_gemv();
 
 void configure_gs_kernels() {
@@ -259,6 +260,7 @@ void configure_gs_kernels() {
   cudaFuncSetAttribute(gs_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   configure_gs_ws();
   configure_gs_diag();
+  configure_gs_macro();
   configure_dense_gemv();
 }
 
