@@ -297,7 +297,7 @@ def run_b200(args, rank, world, local_rank):
     gs_bytes = 24 * p0.n_internal
     gs_avg_s = gs_ms / max(gs_n, 1) / 1e3
     achieved = gs_bytes / gs_avg_s / 1e9 if gs_n else None
-    roofline = {"bound": "hbm", "kernel": "gs_diag_kernel<3> (finest level GS-LEX sweep)",
+    roofline = {"bound": "hbm", "kernel": "gs_macro_kernel (finest level GS-LEX sweep, 3-D two-chain)" if not os.environ.get("GMG_GS_MACRO", "1") == "0" else "gs_diag_kernel<3> (finest level GS-LEX sweep)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(),
                 "algorithmic_bytes_per_launch": gs_bytes, "avg_launch_ms": gs_avg_s * 1e3,
