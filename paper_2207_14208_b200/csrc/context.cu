@@ -952,6 +952,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_VARIANT")) ctx->gs_variant = atoi(e);
   if (const char* e = getenv("GMG_GS_HALO")) ctx->halo_multi = atoi(e);
   if (const char* e = getenv("GMG_GS_MACRO")) ctx->gs_macro = atoi(e);
+  if (const char* e = getenv("GMG_GS_MACRO_CTAS")) ctx->macro_ctas = atoi(e);  // timing experiments only
   if (const char* e = getenv("GMG_BAND_COOP")) ctx->band_coop_max = atoll(e);
   if (const char* e = getenv("GMG_GHOST_BPS")) ctx->ghost_bps = std::max(1, atoi(e));
   if (const char* e = getenv("GMG_GHOST_RAW")) ctx->ghost_raw_only = e[0] != '0';

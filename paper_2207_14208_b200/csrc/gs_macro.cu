@@ -80,10 +80,19 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
     __syncthreads();
     const int tid = S.task;
     if (tid >= a.ntasks) return;
+    // diagnostics (GMG_GS_TRACE=1): [0] claim, [1] done, [2] SM, [4] compute-warp cycles
+    long long* const tr = a.trace ? a.trace + (int64_t)tid * 24 : nullptr;
+    if (tr && threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tr[0] = gtimer();
+      tr[2] = smid;
+    }
     const int2 tk = a.tasks[tid];
     const int c = tk.x, b = tk.y;
     if (a.empty && a.empty[tid]) {
       if (threadIdx.x == 0) st_relaxed(a.progress + 4 * (c * a.Bn + b), nM);
+      if (tr && threadIdx.x == 0) tr[1] = gtimer();
       __syncthreads();
       continue;
     }
@@ -134,6 +143,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
       double mA = 0.0, mB = 0.0;  // this lane's results of the previous step
       int r0 = 0;                                // ring row of step 8k
       int f0 = lane == 0 ? 0 : MRF - lane;       // f slot of macro-line 8k - lane
+      const long long c0 = clock64();
       wait_batch(0);
       stage(urow(0), urow(1), urow(MRU - 8), urow(8), f0, ((0 - lane) & 7) == 7);
       for (int k = 0; k < NCq; ++k) {
@@ -180,6 +190,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
         __syncwarp();
         if (lane == 0) st_flag(&S.cons, 8 * k + 7);
       }
+      if (tr && lane == 0) tr[4] = clock64() - c0;
     } else if (warp == 1) {
       // ============================ u loader =============================
       // cp.async of the task's own columns (old values: computed rows and the
@@ -390,6 +401,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
         ++w;
       }
       if (lane == 0) bulk_wait<0>();
+      if (tr && lane == 0) tr[1] = gtimer();
     }
     __syncthreads();
   }
