@@ -159,7 +159,10 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
           const double c_hfA = hfA, c_hfB = hfB, c_oA = oA, c_oB = oB;
           const uint32_t c_mwA = mwA, c_mwB = mwB;
           const bool first = ((i - lane) & 7) == 0;  // this lane's macro-line has i = 0
-          if (i == 7 && k + 1 < NCq) wait_batch(k + 1);
+          if (i == 7 && k + 1 < NCq) {
+            wait_batch(k + 1);
+            if (tr && lane == 0 && (k + 1 == 64 || k + 1 == 512)) tr[k + 1 == 64 ? 8 : 11] = gtimer();
+          }
           {  // stage step 8k + i + 1
             const unsigned own1 = i < 7 ? cb + (unsigned)(i + 1) * MRBY : nb;
             const unsigned nx1 = i < 6 ? cb + (unsigned)(i + 2) * MRBY : (i == 6 ? nb : nb + MRBY);
@@ -189,6 +192,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
         f0 = fslot(f0 + 8);
         __syncwarp();
         if (lane == 0) st_flag(&S.cons, 8 * k + 7);
+        if (tr && lane == 0 && k == 68) tr[10] = gtimer();
       }
       if (tr && lane == 0) tr[4] = clock64() - c0;
     } else if (warp == 1) {
@@ -313,6 +317,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
         return !(uprog && seenU < needU);
       };
       auto issue = [&](int h, double& hv, double& uw) {
+        if (tr && h == 64 && lane == 0) tr[6] = gtimer();
         hv = uw = 0.0;
         const int plane = hsl == 0 ? h + 1 : h;
         const int r = 8 * hsl + hil;
@@ -329,6 +334,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
         if (h + 1 <= N - 1) S.u[umod(8 * h + lane, MRU)][0][lane + 1] = uw;  // (8h, A, ci = lane + 1)
         __syncwarp();
         if (lane == 0) st_flag(&S.hready, h + 1);
+        if (tr && h == 64 && lane == 0) tr[7] = gtimer();
       };
       int hs = 0, hi = 0;  // next batch to store / to issue
       double hvA = 0.0, uwA = 0.0, hvB = 0.0, uwB = 0.0;
@@ -370,6 +376,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
           __nanosleep(a.sleep_ns[3]);
           continue;
         }
+        if (tr && w == 64 && lane == 0) tr[9] = gtimer();
         if (lane == 0) bulk_wait_read<0>();  // staging free
         __syncwarp();
 #pragma unroll
@@ -396,6 +403,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
             bulk_wait<0>();  // this batch's lines are in L2
           }
           st_relaxed(myprog, 8 * w + 8);
+          if (tr && (w == 64 || w == 65)) tr[w == 64 ? 5 : 12] = gtimer();
         }
         __syncwarp();
         ++w;

@@ -72,3 +72,25 @@ running = [int(((st <= t) & (en > t)).sum()) for t in grid]
 print("running tasks over time:", " ".join(f"{t:.0f}:{r}" for t, r in zip(grid, running)))
 last = np.argsort(en)[-5:]
 print("last-ending tasks (c, b, start, end):", [(tasks[i], round(st[i], 1), round(en[i], 1)) for i in last])
+
+# hand-off decomposition at batch 64 (trace words: 10 upstream compute done with
+# batch 68 (writer batch 64 becomes final), 9 writer notices it, 5 / 12 progress
+# 520 / 528 issued, 6 downstream halo loader issues batch 64, 7 halo stored,
+# 8 downstream compute starts batch 64, 11 compute starts batch 512)
+idx = {t: i for i, t in enumerate(tasks)}
+rate = (tr[:, 11] - tr[:, 8]) / (448 * 8.0)
+ok = (tr[:, 8] > 0) & (tr[:, 11] > 0)
+print(f"compute ns/step between batches 64 and 512: median {np.median(rate[ok]):.0f} (min {rate[ok].min():.0f}, max {rate[ok].max():.0f})")
+for kind, du in (("c-hop", (-1, 0)), ("b-hop", (0, -1))):
+    rows = []
+    for (c, b), i in idx.items():
+        up = idx.get((c + du[0], b + du[1]))
+        if up is None or tr[i, 8] == 0 or tr[up, 10] == 0:
+            continue
+        pub = tr[up, 5] if kind == "c-hop" else tr[up, 12]
+        rows.append([tr[up, 9] - tr[up, 10], pub - tr[up, 9], tr[i, 6] - pub, tr[i, 7] - tr[i, 6],
+                     tr[i, 8] - tr[i, 7], tr[i, 8] - tr[up, 8]])
+    r = np.median(np.array(rows), axis=0) / 1e3
+    print(f"{kind} (us, median of {len(rows)}): upstream batch final -> writer notices {r[0]:.2f}; -> flag {r[1]:.2f}; "
+          f"-> downstream halo issue {r[2]:.2f}; -> halo stored {r[3]:.2f}; -> compute starts {r[4]:.2f}; "
+          f"batch-64 start lag {r[5]:.2f}")
