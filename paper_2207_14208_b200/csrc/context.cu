@@ -170,6 +170,7 @@ struct gmg_ctx {
   int gs_sleep[4] = {500, 500, 20, 200};  // GS loader / writer back-off (ns), GMG_GS_SLEEP=u,f,h,w  // one launch per ghost batch instead of the persistent sweep
   int ws_ctas_per_sm = 4;
   int gs_macro = 1;            // 3-D GS: two line chains per lane (gs_macro.cu; GMG_GS_MACRO=0: gs_diag.cu)
+  int gs_pstride = 32;         // ints between progress words: one 128-byte line per task (GMG_GS_PSTRIDE=4: 16 B)
   int macro_ctas = 0;          // its resident CTAs per SM (occupancy query on first use)
   bool prof = false;
   int prof_mask = 0;   // bit k: time kernel class k
@@ -477,7 +478,7 @@ int gs_grid(const DevLevel& l) {
 // ---- operations ------------------------------------------------------------
 int op_gs(gmg_ctx* ctx, DevLevel& l) {
   Scope s(ctx, 0);
-  GMG_CHECK(ctx, cudaMemsetAsync(l.progress, 0, sizeof(int) * (size_t)(4 * l.C * l.Bn + 4), ctx->stream));
+  GMG_CHECK(ctx, cudaMemsetAsync(l.progress, 0, sizeof(int) * (size_t)(32 * l.C * l.Bn + 4), ctx->stream));
   GsArgs a;
   a.g = l.g;
   a.labels = l.labels;
@@ -488,6 +489,7 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
   a.ntasks = l.ntasks;
   a.ticket = l.ticket;
   a.progress = l.progress;
+  a.pstride = ctx->gs_pstride;
   a.B1 = l.B1;
   a.Bn = l.Bn;
   a.C = l.C;
@@ -952,6 +954,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_VARIANT")) ctx->gs_variant = atoi(e);
   if (const char* e = getenv("GMG_GS_HALO")) ctx->halo_multi = atoi(e);
   if (const char* e = getenv("GMG_GS_MACRO")) ctx->gs_macro = atoi(e);
+  if (const char* e = getenv("GMG_GS_PSTRIDE")) ctx->gs_pstride = atoi(e) >= 32 ? 32 : 4;
   if (const char* e = getenv("GMG_GS_MACRO_CTAS")) ctx->macro_ctas = atoi(e);  // timing experiments only
   if (const char* e = getenv("GMG_BAND_COOP")) ctx->band_coop_max = atoll(e);
   if (const char* e = getenv("GMG_GHOST_BPS")) ctx->ghost_bps = std::max(1, atoi(e));
@@ -1297,9 +1300,9 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   if (upload(ctx, &l.tempty, tempty.data(), (int64_t)tempty.size())) return -1;
   // progress words: 16 B per task (the TMA-store path writes them with bulk copies);
   // the older kernels use the first C * Bn ints
-  if (upload(ctx, &l.tasks, tasks.data(), l.ntasks) || dalloc(ctx, &l.progress, 4 * l.C * l.Bn + 4))
+  if (upload(ctx, &l.tasks, tasks.data(), l.ntasks) || dalloc(ctx, &l.progress, 32 * l.C * l.Bn + 4))
     return -1;
-  l.ticket = l.progress + 4 * l.C * l.Bn;
+  l.ticket = l.progress + 32 * l.C * l.Bn;
 
   // coarsest direct-solve ordering: internal then ghost (ref operators.py:180)
   if (li == ctx->nlevels - 1) {

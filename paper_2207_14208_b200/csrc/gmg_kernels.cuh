@@ -16,7 +16,8 @@ struct GsArgs {
   const uint8_t* empty;  // gs_diag: task without internal nodes (published as done at once), or null
   int ntasks;
   int* ticket;
-  int* progress;      // [C * Bn] completed lines per task
+  int* progress;      // completed lines per task, at progress[pstride * (c * Bn + b)]
+  int pstride;        // ints between two tasks' progress words (4 or 32: one 128-byte line each)
   int B1, Bn, C;
   const uint32_t* imask;  // per (line, chunk) bitmask of internal nodes, row stride Cm
   int Cm;                 // C rounded up to a multiple of 4

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
       // read its columns / rows as they are
       if (threadIdx.x == 0) {
         const int nl = D == 3 ? (N - 1) * PL : ((N + 1 + 7) & ~7);
-        st_relaxed(a.progress + 4 * (c * a.Bn + b), nl);
+        st_relaxed(a.progress + a.pstride * (c * a.Bn + b), nl);
       }
       __syncthreads();
       continue;
@@ -461,8 +461,8 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         // coupling (tools/gs_tune.py).
         if (a.variant >= 1000) {
           const int X = a.variant - 1000;
-          const int* lp = c > 0 ? a.progress + 4 * ((c - 1) * a.Bn + b) : nullptr;
-          const int* up = (D == 3 && b > 0) ? a.progress + 4 * (c * a.Bn + (b - 1)) : nullptr;
+          const int* lp = c > 0 ? a.progress + a.pstride * ((c - 1) * a.Bn + b) : nullptr;
+          const int* up = (D == 3 && b > 0) ? a.progress + a.pstride * (c * a.Bn + (b - 1)) : nullptr;
           while ((lp && ld_relaxed(lp) < min(X, nLines)) || (up && ld_relaxed(up) < min(X, nLines))) __nanosleep(200);
         }
         for (int h = 0; h < NHq; ++h) {
@@ -481,8 +481,8 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         // block (new values of task b-1).  Two batches in flight: the loads of
         // batch h+1 are issued before batch h's values are stored, so one L2
         // latency is overlapped with the next poll.
-        const int* lprog = c > 0 ? a.progress + 4 * ((c - 1) * a.Bn + b) : nullptr;
-        const int* uprog = (D == 3 && b > 0) ? a.progress + 4 * (c * a.Bn + (b - 1)) : nullptr;
+        const int* lprog = c > 0 ? a.progress + a.pstride * ((c - 1) * a.Bn + b) : nullptr;
+        const int* uprog = (D == 3 && b > 0) ? a.progress + a.pstride * (c * a.Bn + (b - 1)) : nullptr;
         int seenL = 0, seenU = 0;
         auto up_line = [&](int h) -> int {  // up-halo pseudo-line loaded with batch h, or -1
           if (D != 3) return -1;
@@ -573,8 +573,8 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         // ready -- up to four batches, one line per lane -- so the loader keeps
         // pace with the compute warp however far the neighbours' publications
         // are behind, instead of paying one round trip per batch.
-        const int* lprog = c > 0 ? a.progress + 4 * ((c - 1) * a.Bn + b) : nullptr;
-        const int* uprog = (D == 3 && b > 0) ? a.progress + 4 * (c * a.Bn + (b - 1)) : nullptr;
+        const int* lprog = c > 0 ? a.progress + a.pstride * ((c - 1) * a.Bn + b) : nullptr;
+        const int* uprog = (D == 3 && b > 0) ? a.progress + a.pstride * (c * a.Bn + (b - 1)) : nullptr;
         int seenL = lprog ? 0 : (1 << 30), seenU = uprog ? 0 : (1 << 30);
         auto up_line = [&](int h) -> int {  // up-halo pseudo-line loaded with batch h, or -1
           if (D != 3) return -1;
@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
       // progress word is itself written by a 16-B bulk store issued only after
       // the data group has completed (wait_group), so publishing needs no
       // memory barrier and overlaps the next batch.
-      int* myprog = a.progress + 4 * (c * a.Bn + b);
+      int* myprog = a.progress + a.pstride * (c * a.Bn + b);
       const int NWq = nLines / 8;
       long long idle = 0, wpub = 0;
       int w = 0;

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
     const int2 tk = a.tasks[tid];
     const int c = tk.x, b = tk.y;
     if (a.empty && a.empty[tid]) {
-      if (threadIdx.x == 0) st_relaxed(a.progress + 4 * (c * a.Bn + b), nM);
+      if (threadIdx.x == 0) st_relaxed(a.progress + a.pstride * (c * a.Bn + b), nM);
       if (tr && threadIdx.x == 0) tr[1] = gtimer();
       __syncthreads();
       continue;
@@ -300,8 +300,8 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
       // block for slot A's i = 0 line (plane h+1, new values of task b-1, whose
       // row 14 of plane h+1 is in its macro batch h+1).  Two batches in
       // flight, as in gs_diag.cu.
-      const int* lprog = c > 0 ? a.progress + 4 * ((c - 1) * a.Bn + b) : nullptr;
-      const int* uprog = b > 0 ? a.progress + 4 * (c * a.Bn + (b - 1)) : nullptr;
+      const int* lprog = c > 0 ? a.progress + a.pstride * ((c - 1) * a.Bn + b) : nullptr;
+      const int* uprog = b > 0 ? a.progress + a.pstride * (c * a.Bn + (b - 1)) : nullptr;
       int seenL = 0, seenU = 0;
       const int hsl = (lane >> 3) & 1, hil = lane & 7;  // lane's halo line: slot, in-batch index
       const bool right = lane >= 16;
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
       // slots go out with one TMA tile store each (A: plane w+1 rows 1-7, B:
       // plane w rows 8-14; rows past row N are clipped, boundary planes are
       // skipped), then the progress word.
-      int* myprog = a.progress + 4 * (c * a.Bn + b);
+      int* myprog = a.progress + a.pstride * (c * a.Bn + b);
       int w = 0;
       while (w < N) {
         const int cs = ld_flag(&S.cons);

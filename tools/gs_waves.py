@@ -35,8 +35,10 @@ for _ in range(3):
     ctx.apply(level, _lib.OP_GS_SWEEP)
 ctx.synchronize()
 ctx.profile(True)
-ctx.apply(level, _lib.OP_GS_SWEEP)
-ms, _ = ctx.profile_read("gs_sweep", level)
+for _ in range(int(os.environ.get("GS_WAVES_REPS", "5"))):
+    ctx.apply(level, _lib.OP_GS_SWEEP)
+ms, nrep = ctx.profile_read("gs_sweep", level)
+ms /= max(nrep, 1)
 ctx.profile(False)
 Nn = p.N
 C = (Nn - 1 + 31) // 32
@@ -53,7 +55,7 @@ en = (tr[:, 1] - t0) / 1e3
 dur = en - st
 sm = tr[:, 2] & 0xFFFF
 diag = np.array([c + b for c, b in tasks])
-print(f"level {level} N={Nn} tasks={nt} C={C} Bn={Bn} sweep {ms:.3f} ms (events), span {en.max():.1f} us, "
+print(f"level {level} N={Nn} tasks={nt} C={C} Bn={Bn} sweep {ms:.3f} ms (events, mean of {nrep}), span {en.max():.1f} us, "
       f"SMs {len(np.unique(sm))}, max tasks/SM {np.bincount(sm).max()}")
 print(f"task duration us: mean {dur.mean():.1f} min {dur.min():.1f} max {dur.max():.1f}; "
       f"compute cycles/step mean {(tr[:, 4] / (8 * Nn + 31)).mean():.0f}")
