@@ -76,6 +76,8 @@ struct DevLevel {
   // Gauss-Seidel tasks
   int2* tasks = nullptr;
   uint8_t* tempty = nullptr;  // per task (list order): no internal node
+  uint8_t* tempty_cb = nullptr;  // the same per task (c * Bn + b)
+  double* edge = nullptr;        // gs_macro row-above hand-off cells (zero between sweeps)
   int ntasks = 0, B1 = 1, Bn = 1, C = 1;
   uint32_t* imask = nullptr;  // streaming GS: internal bitmask per (line, chunk)
   uint32_t* imask2 = nullptr; // diagonal GS (3-D): masks per (plane, block, pseudo-line)
@@ -170,6 +172,7 @@ struct gmg_ctx {
   int gs_sleep[4] = {500, 500, 20, 200};  // GS loader / writer back-off (ns), GMG_GS_SLEEP=u,f,h,w  // one launch per ghost batch instead of the persistent sweep
   int ws_ctas_per_sm = 4;
   int gs_macro = 1;            // 3-D GS: two line chains per lane (gs_macro.cu; GMG_GS_MACRO=0: gs_diag.cu)
+  bool gs_edge = false;        // gs_macro: per-cell row-above hand-off (GMG_GS_EDGE=1; measured slower)
   int gs_pstride = 32;         // ints between progress words: one 128-byte line per task (GMG_GS_PSTRIDE=4: 16 B)
   int macro_ctas = 0;          // its resident CTAs per SM (occupancy query on first use)
   bool prof = false;
@@ -257,7 +260,7 @@ void free_level(DevLevel& l) {
   free_tree(l.l2g);
   void* ptrs[] = {l.labels, l.u, l.f, l.rI, l.rE, l.gnode, l.gbase, l.gw, l.gdtau, l.gval, l.gtmp,
                   l.gprom, l.slot2lex, l.lex2slot, l.band_idx, l.bfs_mask, l.tstep, l.tabsn,
-                  l.bscratch, l.tasks, l.tempty, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
+                  l.bscratch, l.tasks, l.tempty, l.tempty_cb, l.edge, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
                   l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off,
                   l.bfixpos, l.bnbr, l.bv0, l.bv1, l.gwl, l.gbasel, l.gnodel, l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g,
                   l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part, l.nd_crow, l.nd_ccol, l.nd_cval};  // ticket lives in progress
@@ -490,6 +493,9 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
   a.ticket = l.ticket;
   a.progress = l.progress;
   a.pstride = ctx->gs_pstride;
+  // per-cell row-above hand-off (gs_macro); partial sweeps (GMG_GS_MAX_TASKS) would leave cells set
+  a.edge = (ctx->gs_edge && ctx->gs_max_tasks <= 0 && ctx->gs_macro) ? l.edge : nullptr;
+  a.empty_cb = l.tempty_cb;
   a.B1 = l.B1;
   a.Bn = l.Bn;
   a.C = l.C;
@@ -954,6 +960,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_VARIANT")) ctx->gs_variant = atoi(e);
   if (const char* e = getenv("GMG_GS_HALO")) ctx->halo_multi = atoi(e);
   if (const char* e = getenv("GMG_GS_MACRO")) ctx->gs_macro = atoi(e);
+  if (const char* e = getenv("GMG_GS_EDGE")) ctx->gs_edge = e[0] == '1';
   if (const char* e = getenv("GMG_GS_PSTRIDE")) ctx->gs_pstride = atoi(e) >= 32 ? 32 : 4;
   if (const char* e = getenv("GMG_GS_MACRO_CTAS")) ctx->macro_ctas = atoi(e);  // timing experiments only
   if (const char* e = getenv("GMG_BAND_COOP")) ctx->band_coop_max = atoll(e);
@@ -1298,6 +1305,20 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   if (l.tempty) cudaFree(l.tempty);
   l.tempty = nullptr;
   if (upload(ctx, &l.tempty, tempty.data(), (int64_t)tempty.size())) return -1;
+  if (l.diag_gs && d == 3) {
+    std::vector<uint8_t> ecb((size_t)l.C * l.Bn, 0);
+    for (size_t t = 0; t < tasks.size(); ++t) ecb[(size_t)tasks[t].x * l.Bn + tasks[t].y] = tempty[t];
+    if (l.tempty_cb) cudaFree(l.tempty_cb);
+    l.tempty_cb = nullptr;
+    if (upload(ctx, &l.tempty_cb, ecb.data(), (int64_t)ecb.size())) return -1;
+    if (l.edge) cudaFree(l.edge);
+    l.edge = nullptr;
+  }
+  if (l.diag_gs && d == 3 && ctx->gs_edge) {
+    const int64_t ne = (int64_t)l.C * l.Bn * (N + 1) * 64;
+    if (dalloc(ctx, &l.edge, ne)) return -1;
+    GMG_CHECK(ctx, cudaMemset(l.edge, 0, sizeof(double) * (size_t)ne));
+  }
   // progress words: 16 B per task (the TMA-store path writes them with bulk copies);
   // the older kernels use the first C * Bn ints
   if (upload(ctx, &l.tasks, tasks.data(), l.ntasks) || dalloc(ctx, &l.progress, 32 * l.C * l.Bn + 4))

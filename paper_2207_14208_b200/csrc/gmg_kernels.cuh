@@ -18,6 +18,9 @@ struct GsArgs {
   int* ticket;
   int* progress;      // completed lines per task, at progress[pstride * (c * Bn + b)]
   int pstride;        // ints between two tasks' progress words (4 or 32: one 128-byte line each)
+  double* edge;       // gs_macro: per-cell hand-off of each block's last row, (value, tag) pairs
+                      // [task c * Bn + b][plane 0..N][32 columns]; all tags zero between sweeps, or null
+  const uint8_t* empty_cb;  // task (c * Bn + b) has no internal node
   int B1, Bn, C;
   const uint32_t* imask;  // per (line, chunk) bitmask of internal nodes, row stride Cm
   int Cm;                 // C rounded up to a multiple of 4

@@ -43,6 +43,25 @@ constexpr unsigned MRBY = 2 * MW * 8;    // ring row bytes
 constexpr unsigned FSB = MRF * 256u;     // byte offset of slot B's f ring
 constexpr unsigned MSB = MRF * 16u;      // byte offset of slot B's mask ring
 
+// Row-above hand-off between blocks b and b+1 (a.edge): lane j of the upper
+// task stores (value, 1) for its column of row 14 of plane p as soon as it has
+// relaxed it; lane j of the lower task's halo loader polls that one cell, puts
+// the value into its ring and clears the cell (every cell is produced and
+// consumed exactly once per sweep, so the buffer is all-zero between sweeps).
+// The lower task then lags the upper one by 14 steps + an L2 round trip instead
+// of waiting for the upper task's writer batch (46 steps + the progress word).
+__device__ __forceinline__ void edge_put(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v), "d"(1.0) : "memory");
+}
+__device__ __forceinline__ double2 edge_get(const double* p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void edge_clear(double* p) {
+  asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %1};" ::"l"(p), "d"(0.0) : "memory");
+}
+
 struct __align__(128) MgSmem {
   double st[2][8][32];        // writer staging (TMA store sources)
   double f[2][MRF][32];       // slot s, macro-line m at [s][m mod MRF]
@@ -51,12 +70,14 @@ struct __align__(128) MgSmem {
   unsigned long long ubar[MNUB];
   unsigned long long fbar[MNFB];
   int uready, fready, hready, cons, wdone, task;
+  int aready[32];  // per column: row-above batches stored by the halo loader (edge mode)
 };
 static_assert(sizeof(MgSmem) <= 75 * 1024, "three CTAs per SM (228 KB incl. 1 KB reserved each)");
 
 }  // namespace
 
-__global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid_constant__ WsMaps maps) {
+template <bool EDGE>
+__global__ void __launch_bounds__(EDGE ? 192 : 160, 3) gs_macro_kernel(GsArgs a, const __grid_constant__ WsMaps maps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   MgSmem& S = *reinterpret_cast<MgSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -75,6 +96,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
       S.hready = 0;
       S.cons = -1;
       S.wdone = 0;
+      for (int i = 0; i < 32; ++i) S.aready[i] = 0;
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -90,7 +112,17 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
     }
     const int2 tk = a.tasks[tid];
     const int c = tk.x, b = tk.y;
+    // this task's row-14 cells for block b+1, and block b-1's cells for this one
+    double* const eout = (EDGE && b + 1 < a.Bn && !a.empty_cb[c * a.Bn + b + 1]) ? a.edge + (int64_t)(c * a.Bn + b) * (N + 1) * 64 : nullptr;
+    double* const ein = (EDGE && b > 0) ? a.edge + (int64_t)(c * a.Bn + b - 1) * (N + 1) * 64 : nullptr;
     if (a.empty && a.empty[tid]) {
+      if (eout) {  // no internal node: row 14 keeps its old values
+        const int64_t r14 = 1 + MRB * b + 13, cc = 1 + 32 * c + (int)OFF;
+        for (int t = threadIdx.x; t < (N - 1) * 32; t += blockDim.x) {
+          const int pl = 1 + (t >> 5), j = t & 31;
+          edge_put(eout + ((int64_t)pl * 32 + j) * 2, __ldcg(a.u + ((int64_t)pl * g.n + r14) * g.P + cc + j));
+        }
+      }
       if (threadIdx.x == 0) st_relaxed(a.progress + a.pstride * (c * a.Bn + b), nM);
       if (tr && threadIdx.x == 0) tr[1] = gtimer();
       __syncthreads();
@@ -117,6 +149,10 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
         while (ld_flag(&S.uready) < cu) __nanosleep(20);
         while (ld_flag(&S.fready) < cf) __nanosleep(20);
         while (ld_flag(&S.hready) < ch) __nanosleep(20);
+        if (EDGE) {  // lane j stages the row above of batch k - j/8 during this batch
+          const int need = min(k - (lane >> 3) + 1, NHq);
+          while (!__all_sync(0xffffffffu, ld_flag(&S.aready[lane]) >= need)) __nanosleep(20);
+        }
       };
       auto urow = [&](int r) -> unsigned { return ub + (unsigned)r * MRBY + lu; };
       auto rmod = [&](int r) -> int { return r < 0 ? r + MRU : (r >= MRU ? r - MRU : r); };
@@ -182,6 +218,11 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
           const double vB = (c_hfB + sB) * inv;
           mA = (c_mwA & mybit) ? vA : c_oA;
           mB = (c_mwB & mybit) ? vB : c_oB;
+          if (EDGE && eout && ((i - lane) & 7) == 6) {  // this lane's B line is row 14 of plane (8k + i - lane) / 8
+            const int mline = 8 * k + i - lane;
+            const int pl = mline >> 3;
+            if (mline >= 0 && pl >= 1 && pl <= N - 1) edge_put(eout + ((int64_t)pl * 32 + lane) * 2, mB);
+          }
           if (8 * k + i - lane < nM + 8) {  // cells past the last loaded line may alias unwritten lines
             sts(cb + (unsigned)i * MRBY, mA);
             sts(cb + (unsigned)i * MRBY + SLOTB, mB);
@@ -301,7 +342,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
       // row 14 of plane h+1 is in its macro batch h+1).  Two batches in
       // flight, as in gs_diag.cu.
       const int* lprog = c > 0 ? a.progress + a.pstride * ((c - 1) * a.Bn + b) : nullptr;
-      const int* uprog = b > 0 ? a.progress + a.pstride * (c * a.Bn + (b - 1)) : nullptr;
+      const int* uprog = (b > 0 && !EDGE) ? a.progress + a.pstride * (c * a.Bn + (b - 1)) : nullptr;
       int seenL = 0, seenU = 0;
       const int hsl = (lane >> 3) & 1, hil = lane & 7;  // lane's halo line: slot, in-batch index
       const bool right = lane >= 16;
@@ -323,7 +364,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
         const int r = 8 * hsl + hil;
         if (plane >= 1 && plane <= N - 1 && r >= 1 && r <= Rb)
           hv = __ldcg(a.u + ((int64_t)plane * g.n + rowbase - 1 + r) * g.P + col0 + (right ? 32 : -1));
-        if (h + 1 <= N - 1) uw = __ldcg(a.u + ((int64_t)(h + 1) * g.n + rowbase - 1) * g.P + col0 + lane);
+        if (!EDGE && h + 1 <= N - 1) uw = __ldcg(a.u + ((int64_t)(h + 1) * g.n + rowbase - 1) * g.P + col0 + lane);
       };
       auto store = [&](int h, double hv, double uw) {
         const int m = 8 * h + hil;
@@ -331,7 +372,7 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
           S.u[umod(m - 1, MRU)][hsl][0] = hv;  // ci = 0
         else
           S.u[umod(m + 32, MRU)][hsl][33] = hv;  // ci = 33
-        if (h + 1 <= N - 1) S.u[umod(8 * h + lane, MRU)][0][lane + 1] = uw;  // (8h, A, ci = lane + 1)
+        if (!EDGE && h + 1 <= N - 1) S.u[umod(8 * h + lane, MRU)][0][lane + 1] = uw;  // (8h, A, ci = lane + 1)
         __syncwarp();
         if (lane == 0) st_flag(&S.hready, h + 1);
         if (tr && h == 64 && lane == 0) tr[7] = gtimer();
@@ -410,6 +451,53 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
       }
       if (lane == 0) bulk_wait<0>();
       if (tr && lane == 0) tr[1] = gtimer();
+    } else if (EDGE && warp == 5) {
+      // ============================ row-above loader (edge mode) ========
+      // Lane j moves the row-above cell of column j for batch ha into ring
+      // cell (8ha, A, ci = j + 1) once block b-1 has relaxed it (or, for the
+      // first block, from the boundary row), then clears the cell.
+      // Up to four batches are polled per L2 round trip (independent loads in
+      // flight), so a lane delivers several batches per round trip once the
+      // upper block is ahead.
+      int ha = 0;
+      auto ring_free = [&](int h) -> bool {
+        const int old = 8 * h + 7 - MRU;
+        if (ld_flag(&S.cons) < old + MDEAD) return false;
+        return !(old >= 0 && ld_flag(&S.wdone) < min(old + 1, nM));
+      };
+      while (ha < NHq) {
+        int nb = 0;
+        while (nb < 4 && ha + nb < NHq && ring_free(ha + nb)) ++nb;
+        if (nb == 0) {
+          __nanosleep(a.sleep_ns[2]);
+          continue;
+        }
+        double2 pv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          pv[q] = make_double2(0.0, 1.0);
+          if (q < nb && ha + q + 1 <= N - 1) {
+            if (ein)
+              pv[q] = edge_get(ein + ((int64_t)(ha + q + 1) * 32 + lane) * 2);
+            else
+              pv[q].x = __ldcg(a.u + ((int64_t)(ha + q + 1) * g.n + rowbase - 1) * g.P + col0 + lane);
+          }
+        }
+        const int h0 = ha;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q >= nb || ha != h0 + q || pv[q].y == 0.0) continue;
+          if (ha + 1 <= N - 1) {
+            if (ein) edge_clear(ein + ((int64_t)(ha + 1) * 32 + lane) * 2);
+            S.u[umod(8 * ha + lane, MRU)][0][lane + 1] = pv[q].x;  // (8ha, A, ci = lane + 1)
+          }
+          ++ha;
+        }
+        if (ha != h0)
+          st_flag(&S.aready[lane], ha);
+        else
+          __nanosleep(a.sleep_ns[2]);
+      }
     }
     __syncthreads();
   }
@@ -418,17 +506,21 @@ __global__ void __launch_bounds__(160, 3) gs_macro_kernel(GsArgs a, const __grid
 size_t gs_macro_smem() { return sizeof(MgSmem); }
 
 void configure_gs_macro() {
-  cudaFuncSetAttribute(gs_macro_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MgSmem));
+  cudaFuncSetAttribute(gs_macro_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MgSmem));
+  cudaFuncSetAttribute(gs_macro_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MgSmem));
 }
 
 int gs_macro_ctas_per_sm() {
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gs_macro_kernel, 160, sizeof(MgSmem)) != cudaSuccess) return 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gs_macro_kernel<false>, 160, sizeof(MgSmem)) != cudaSuccess) return 1;
   return n > 0 ? n : 1;
 }
 
 void launch_gs_macro(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st) {
-  gs_macro_kernel<<<grid, 160, sizeof(MgSmem), st>>>(a, maps);
+  if (a.edge)
+    gs_macro_kernel<true><<<grid, 192, sizeof(MgSmem), st>>>(a, maps);
+  else
+    gs_macro_kernel<false><<<grid, 160, sizeof(MgSmem), st>>>(a, maps);
 }
 
 }  // namespace gmg

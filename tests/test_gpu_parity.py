@@ -235,3 +235,20 @@ def test_batched_solves_match_individual(gpu_available):
     rho_want = [measure_rho(s, seed=42).residual_norms for s in solvers]
     rho_got = [r.residual_norms for r in measure_rho_batched(solvers, seed=42)]
     assert rho_got == rho_want
+
+
+@pytest.mark.parametrize("edge", ["0", "1"])
+def test_gs_variants_pores64_match_reference(edge, gpu_available, monkeypatch):
+    """The opt-in per-cell row-above hand-off of the 3-D GS kernel
+    (GMG_GS_EDGE=1) and the default batch hand-off give the reference's
+    solve bit for bit (pores 64^3: empty tasks, all levels on gs_macro)."""
+    monkeypatch.setenv("GMG_GS_EDGE", edge)
+    rec = GU.record("pores64")
+    plans, solver = _pores64_solver("superlu")
+    u, rep = solver.solve(u=np.zeros(plans[0].n_nodes), cycles=rec["cycles"])
+    assert rep.residual_norms == GU.hexlist(rec["solve"]["residual_norms"])
+    assert GU.digest(u) == rec["solve"]["u_digest"]
+    # a second solve on the same context: the hand-off cells must be clean again
+    u2, rep2 = solver.solve(u=np.zeros(plans[0].n_nodes), cycles=rec["cycles"])
+    assert rep2.residual_norms == rep.residual_norms
+    assert GU.digest(u2) == rec["solve"]["u_digest"]

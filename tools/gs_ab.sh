@@ -1,3 +1,7 @@
-for cfg in "" "GMG_GS_PSTRIDE=32" "GMG_GS_SLEEP=500,500,0,50" "GMG_GS_PSTRIDE=32 GMG_GS_SLEEP=500,500,0,50"; do
-  echo "== $cfg"; env $cfg python tools/gs_waves.py c4:512 0 2>&1 | grep -E "sweep|hop|ns/step"
+#!/bin/bash
+# A/B of GS knobs on the finest 512^3 sweep (tools/gs_waves.py): CONFIGS holds
+# ';'-separated env assignments (empty entry = defaults).
+IFS=';' read -ra CFGS <<< "${CONFIGS:-;GMG_GS_PSTRIDE=4}"
+for cfg in "${CFGS[@]}"; do
+  echo "== $cfg"; env $cfg python tools/gs_waves.py c4:512 ${LEVEL:-0} 2>&1 | grep -E "sweep|hop|ns/step|duration"
 done
