@@ -174,7 +174,8 @@ struct gmg_ctx {
   int gs_macro = 1;            // 3-D GS: two line chains per lane (gs_macro.cu; GMG_GS_MACRO=0: gs_diag.cu)
   bool gs_edge = false;        // gs_macro: per-cell row-above hand-off (GMG_GS_EDGE=1; measured slower)
   int gs_pstride = 32;         // ints between progress words: one 128-byte line per task (GMG_GS_PSTRIDE=4: 16 B)
-  int macro_ctas = 0;          // its CTAs per SM (0: min(2, occupancy) on first use; GMG_GS_MACRO_CTAS)
+  int macro_ctas = 0;          // its CTAs per SM (GMG_GS_MACRO_CTAS; 0: by task count)
+  int macro_occ = 0;           // its resident CTAs per SM (occupancy query on first use)
   bool prof = false;
   int prof_mask = 0;   // bit k: time kernel class k
   int cur_level = -1;  // level tag for profiling records
@@ -512,10 +513,13 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
   }
   if (ctx->gs_max_tasks > 0) a.ntasks = std::min(a.ntasks, ctx->gs_max_tasks);  // timing experiments only
   if (l.diag_gs && l.g.d == 3 && ctx->gs_macro) {
-    // two resident tasks per SM: fewer slots than tasks at 512^3 (296 of 592) but each
-    // steps faster than with three (1.34 vs 1.36 ms, profiles/r01k_gs_ctas_ab.txt)
-    if (ctx->macro_ctas <= 0) ctx->macro_ctas = std::min(2, gs_macro_ctas_per_sm());
-    launch_gs_macro(a, l.maps, std::min(a.ntasks, ctx->macro_ctas * ctx->sms), ctx->stream);
+    // CTAs per SM: two up to ~1000 tasks (512^3: 296 slots for 592 tasks, but each
+    // steps faster than with three: 1.34 vs 1.36 ms), all that fit above (1024^3,
+    // 2368 tasks: 8.65 ms at three vs 8.96 at two; profiles/r01k_gs_ctas_ab.txt)
+    if (ctx->macro_occ <= 0) ctx->macro_occ = gs_macro_ctas_per_sm();
+    const int per_sm = ctx->macro_ctas > 0 ? ctx->macro_ctas
+                                           : (a.ntasks > 1000 ? ctx->macro_occ : std::min(2, ctx->macro_occ));
+    launch_gs_macro(a, l.maps, std::min(a.ntasks, per_sm * ctx->sms), ctx->stream);
   } else if (l.diag_gs)
     launch_gs_diag(a, l.maps, std::min(a.ntasks, ctx->ws_ctas_per_sm * ctx->sms), ctx->stream);
   else if (l.ws_gs)
