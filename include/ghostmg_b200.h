@@ -127,7 +127,11 @@ int gmg_coarse_prog_csr(gmg_ctx *ctx, int64_t m, int64_t k, const int64_t *rowpt
                         const double *val, int64_t x_off, int64_t y0_off, int64_t y_off);
 int gmg_coarse_prog_end(gmg_ctx *ctx, int64_t x_off);
 
-/* Host <-> device copies of a level vector (see enum gmg_vector). */
+/* Host <-> device copies of a level vector (see enum gmg_vector).  The host
+ * array must hold exactly gmg_vector_length(ctx, level, which) doubles
+ * (the reference raises IndexError on a wrongly sized u; the Python binding
+ * checks the length before every copy). */
+int64_t gmg_vector_length(const gmg_ctx *ctx, int level, int which);
 int gmg_set_vector(gmg_ctx *ctx, int level, int which, const double *host);
 int gmg_get_vector(gmg_ctx *ctx, int level, int which, double *host);
 /* Device address of a level vector (valid for the context's lifetime).  Grids

@@ -49,6 +49,7 @@ SIGNATURES = {
     "gmg_set_vector": (_i, [_p, _i, _i, _p]),
     "gmg_get_vector": (_i, [_p, _i, _i, _p]),
     "gmg_device_pointer": (_p, [_p, _i, _i]),
+    "gmg_vector_length": (_i64, [_p, _i, _i]),
     "gmg_apply": (_i, [_p, _i, _i, _i]),
     "gmg_cycle": (_i, [_p, _i]),
     "gmg_residual_norm": (_i, [_p, _i, _p]),
@@ -210,11 +211,22 @@ class Context:
         self.check(self.lib.gmg_set_stream(self.ctx, stream_handle))
 
     # -- vectors --------------------------------------------------------
+    def vector_length(self, level, which):
+        n = int(self.lib.gmg_vector_length(self.ctx, level, which))
+        if n < 0:
+            raise GmgError(f"no vector {which} on level {level}")
+        return n
+
     def set_vector(self, level, which, host):
         host = np.ascontiguousarray(host, dtype=np.float64)
+        n = self.vector_length(level, which)
+        if host.ndim != 1 or host.size != n:
+            raise ValueError(f"vector {which} of level {level} has {n} entries, got an array of shape {host.shape}")
         self.check(self.lib.gmg_set_vector(self.ctx, level, which, ptr(host)))
 
     def get_vector(self, level, which, n, out=None):
+        if n != self.vector_length(level, which):
+            raise ValueError(f"vector {which} of level {level} has {self.vector_length(level, which)} entries, not {n}")
         if out is None:
             out = np.empty(n, dtype=np.float64)
         elif out.shape != (n,) or out.dtype != np.float64 or not out.flags.c_contiguous:

@@ -25,7 +25,6 @@ struct GsArgs {
   const uint32_t* imask;  // per (line, chunk) bitmask of internal nodes, row stride Cm
   int Cm;                 // C rounded up to a multiple of 4
   long long* trace;       // diagnostics: [ntasks][16] timeline per task, or null
-  int variant;            // diagnostics: GS implementation variant (GMG_GS_VARIANT)
   int sleep_ns[4];        // back-off of the u / f / halo loaders and the writer when idle
   int halo_multi;         // gs_diag: halo loader issues up to 4 ready batches per poll (levels with
                           // at most ~1 task per SM; the 2-batch loader is faster when 4 share an SM)
@@ -67,8 +66,6 @@ struct WsMaps {
   CUtensorMap m2;  // 3-D: internal-node masks per (plane, block, pseudo-line), zero on halo lines
   CUtensorMap ust; // u as (plane, row, col) with 7-row boxes (3-D) / (row, col) 8-row boxes (2-D), TMA stores
 };
-void launch_gs_ws(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st);
-size_t gs_ws_smem();
 void launch_gs_diag(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st);
 size_t gs_diag_smem();
 void launch_gs_macro(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st);

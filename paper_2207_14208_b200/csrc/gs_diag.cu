@@ -452,29 +452,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
         (void)leadF;
       }
     } else if (warp == 2) {
-      if (a.variant == 7 || a.variant >= 1000) {
-        // DIAGNOSTIC ONLY (wrong results): publish every halo batch as soon as
-        // its ring cells are free, without waiting for the neighbours or
-        // loading anything -- the sweep time without halo costs (variant 7).
-        // Variant 1000 + X first waits until both neighbours have published X
-        // lines: the wavefront's start stagger without its steady-state
-        // coupling (tools/gs_tune.py).
-        if (a.variant >= 1000) {
-          const int X = a.variant - 1000;
-          const int* lp = c > 0 ? a.progress + a.pstride * ((c - 1) * a.Bn + b) : nullptr;
-          const int* up = (D == 3 && b > 0) ? a.progress + a.pstride * (c * a.Bn + (b - 1)) : nullptr;
-          while ((lp && ld_relaxed(lp) < min(X, nLines)) || (up && ld_relaxed(up) < min(X, nLines))) __nanosleep(200);
-        }
-        for (int h = 0; h < NHq; ++h) {
-          const int old = 8 * h + 7 - RU;
-          for (;;) {
-            const int cs = ld_flag(&S.cons);
-            if (cs >= old + DEADLAG && (old < 0 || ld_flag(&S.wdone) >= min(old + 1, nLines))) break;
-            __nanosleep(100);
-          }
-          if (lane == 0) st_flag(&S.hready, h + 1);
-        }
-      } else if (!a.halo_multi) {
+      if (!a.halo_multi) {
         // ============================ halo loader ==========================
         // Per 8-line batch h: left halo (column k0-1, new values of task c-1),
         // right halo (column k0+32, old) and, once per plane, the row above the
@@ -701,23 +679,10 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
             }
             bulk_commit();
             const long long c0 = tr ? clock64() : 0;
-            if (a.variant == 1) {
-              bulk_wait<1>();  // everything but this batch's stores has completed
-              if (tr) wpub += clock64() - c0;
-              if (w > 0) {
-                int* fl = S.flag[w & 1];
-                fl[0] = 8 * w;  // lines < 8w are in memory
-                if (tr && w == 65) tr[11] = gtimer();
-                fence_async_shared();
-                bulk_store(myprog, sa(fl), 16u);
-                bulk_commit();
-              }
-            } else {
-              bulk_wait<0>();  // this batch's lines are in L2
-              if (tr) wpub += clock64() - c0;
-              if (tr && w == 64) tr[11] = gtimer();
-              st_relaxed(myprog, 8 * w + 8);
-            }
+            bulk_wait<0>();  // this batch's lines are in L2
+            if (tr) wpub += clock64() - c0;
+            if (tr && w == 64) tr[11] = gtimer();
+            st_relaxed(myprog, 8 * w + 8);
           }
           __syncwarp();
           ++w;
@@ -730,16 +695,7 @@ __global__ void __launch_bounds__(160, 4) gs_diag_kernel(GsArgs a, const __grid_
       }
       if (lane == 0) {
         bulk_wait<0>();
-        if (a.variant == 1) {
-          int* fl = S.flag[NWq & 1];
-          fl[0] = nLines;
-          fence_async_shared();
-          bulk_store(myprog, sa(fl), 16u);
-          bulk_commit();
-          bulk_wait<0>();
-        } else {
-          st_relaxed(myprog, nLines);
-        }
+        st_relaxed(myprog, nLines);
       }
       if (tr && lane == 0) tr[13] = wpub;
       (void)idle;

@@ -249,7 +249,6 @@ __global__ void __launch_bounds__(32) gs_stream_kernel(GsArgs a) {
 
 size_t gs_stream_smem_per_warp() { return sizeof(WarpRing); }
 
-void configure_gs_ws();
 void configure_gs_diag();
 void configure_gs_macro();
 void configure_dense_gemv();
@@ -258,7 +257,6 @@ void configure_gs_kernels() {
   const int smem = (int)sizeof(WarpRing);  // one warp per CTA
   cudaFuncSetAttribute(gs_stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(gs_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  configure_gs_ws();
   configure_gs_diag();
   configure_gs_macro();
   configure_dense_gemv();

@@ -237,12 +237,16 @@ def test_batched_solves_match_individual(gpu_available):
     assert rho_got == rho_want
 
 
-@pytest.mark.parametrize("edge", ["0", "1"])
-def test_gs_variants_pores64_match_reference(edge, gpu_available, monkeypatch):
+@pytest.mark.parametrize("edge,grid", [("0", "0"), ("1", "0"), ("0", "1"), ("0", "3"), ("1", "3")])
+def test_gs_variants_pores64_match_reference(edge, grid, gpu_available, monkeypatch):
     """The opt-in per-cell row-above hand-off of the 3-D GS kernel
     (GMG_GS_EDGE=1) and the default batch hand-off give the reference's
-    solve bit for bit (pores 64^3: empty tasks, all levels on gs_macro)."""
+    solve bit for bit (pores 64^3: empty tasks, all levels on gs_macro).
+    GMG_GS_GRID caps the GS grid so that every CTA loops over several task
+    tickets (re-initialising its barriers and reusing its shared-memory rings
+    with stale data from the previous task), as at 512^3 and 1024^3."""
     monkeypatch.setenv("GMG_GS_EDGE", edge)
+    monkeypatch.setenv("GMG_GS_GRID", grid)
     rec = GU.record("pores64")
     plans, solver = _pores64_solver("superlu")
     u, rep = solver.solve(u=np.zeros(plans[0].n_nodes), cycles=rec["cycles"])
