@@ -88,6 +88,13 @@ struct DevLevel {
   bool diag_gs = false;       // lane-diagonal ring kernel (production, N >= 64)
   WsMaps maps;                // its tensor maps (u, f, imask)
   int *progress = nullptr, *ticket = nullptr;
+  // gs_rows.cu (3-D, production): row-per-warp tasks, cells between tasks
+  bool rows_gs = false;
+  int2 *rw_tasks = nullptr, *rw_prange = nullptr;
+  int rw_ntasks = 0, rw_C = 0, rw_Bn = 0;
+  double2 *bcell = nullptr, *ccell = nullptr;
+  int* rw_ctl = nullptr;
+  RowMaps rmaps;
   // coarsest direct solve
   int64_t n_int = 0;
   int64_t* active = nullptr;  // internal nodes then ghost nodes (lex)
@@ -159,6 +166,7 @@ struct gmg_ctx {
   bool ghost_batched = false;
   bool gs_trace = false;       // record the GS task timeline (GMG_GS_TRACE=1)
   int gs_grid_cap = 0;         // > 0: at most this many GS CTAs (tests the multi-task loop)
+  int gs_rows = 1;             // 3-D levels N >= 64: gs_rows.cu (GMG_GS_ROWS=0: gs_macro.cu, same results)
   int64_t band_coop_max = 200000;  // band extensions up to this many nodes: one cooperative launch (GMG_BAND_COOP;
                                    // 128^3 49 -> 40 us, 64^3 47 -> 30 us; 256^3 (533 k nodes) was slower)
   int halo_multi = -1;         // GS halo loader: -1 by level size, 0 two-batch, 1 multi-batch (GMG_GS_HALO)
@@ -262,7 +270,8 @@ void free_level(DevLevel& l) {
                   l.bscratch, l.tasks, l.tempty, l.tempty_cb, l.edge, l.progress, l.active, l.rhs_d, l.x_d, l.imask, l.imask2, l.cinv, l.cpart,
                   l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off,
                   l.bfixpos, l.bnbr, l.bv0, l.bv1, l.gwl, l.gbasel, l.gnodel, l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g,
-                  l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part, l.nd_crow, l.nd_ccol, l.nd_cval};  // ticket lives in progress
+                  l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part, l.nd_crow, l.nd_ccol, l.nd_cval,
+                  l.rw_tasks, l.rw_prange, l.bcell, l.ccell, l.rw_ctl};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -484,6 +493,22 @@ int gs_cap(const gmg_ctx* ctx, int grid) { return ctx->gs_grid_cap > 0 ? std::mi
 // ---- operations ------------------------------------------------------------
 int op_gs(gmg_ctx* ctx, DevLevel& l) {
   Scope s(ctx, 0);
+  if (l.rows_gs) {
+    GsRowArgs r;
+    r.g = l.g;
+    r.u = l.u;
+    r.tasks = l.rw_tasks;
+    r.prange = l.rw_prange;
+    r.ntasks = l.rw_ntasks;
+    r.C = l.rw_C;
+    r.Bn = l.rw_Bn;
+    r.ctl = l.rw_ctl;
+    r.bcell = l.bcell;
+    r.ccell = l.ccell;
+    launch_gs_rows(r, l.rmaps, gs_cap(ctx, std::min(l.rw_ntasks, ctx->sms)), ctx->stream);
+    ctx->launches++;
+    return 0;
+  }
   GMG_CHECK(ctx, cudaMemsetAsync(l.progress, 0, sizeof(int) * (size_t)(32 * l.C * l.Bn + 4), ctx->stream));
   GsArgs a;
   a.g = l.g;
@@ -960,6 +985,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_TRACE")) ctx->gs_trace = e[0] == '1';
   if (const char* e = getenv("GMG_GS_EDGE")) ctx->gs_edge = e[0] == '1';
   if (const char* e = getenv("GMG_GS_GRID")) ctx->gs_grid_cap = atoi(e);  // cap on GS CTAs (multi-task loop test)
+  if (const char* e = getenv("GMG_GS_ROWS")) ctx->gs_rows = atoi(e);       // 0: previous GS kernel (bitwise same)
 #ifdef GMG_EXPERIMENTS
   if (const char* e = getenv("GMG_SIMPLE_GS")) ctx->force_simple_gs = e[0] == '1';
   if (const char* e = getenv("GMG_NO_WS")) ctx->no_ws = e[0] == '1';
@@ -1332,6 +1358,55 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   if (upload(ctx, &l.tasks, tasks.data(), l.ntasks) || dalloc(ctx, &l.progress, 32 * l.C * l.Bn + 4))
     return -1;
   l.ticket = l.progress + 32 * l.C * l.Bn;
+
+  // gs_rows.cu tasks (3-D, N >= 64): chunk c x block of GS_ROWS rows; per task
+  // the planes that hold internal nodes; tickets ordered by 3c + b (each task
+  // after its two upstream tasks; a column hop lags ~3x a row hop)
+  l.rows_gs = false;
+  if (d == 3 && N >= 64 && ctx->gs_rows && l.diag_gs && !empty_im.empty()) {
+    const int R = gs_rows_rows();
+    const int C = l.C, Bn = (int)((N - 1 + R - 1) / R);
+    const int64_t n = N + 1;
+    std::vector<int2> pr((size_t)C * Bn, make_int2(1 << 30, -1));
+    for (int64_t p = 1; p <= N - 1; ++p)
+      for (int64_t row = 1; row <= N - 1; ++row) {
+        const uint32_t* wrow = &empty_im[(size_t)((p * n + row) * l.Cm)];
+        const int b = (int)((row - 1) / R);
+        for (int c = 0; c < C; ++c)
+          if (wrow[c]) {
+            int2& q = pr[(size_t)c * Bn + b];
+            q.x = std::min<int>(q.x, (int)p);
+            q.y = std::max<int>(q.y, (int)p);
+          }
+      }
+    std::vector<int2> rt;
+    rt.reserve((size_t)C * Bn);
+    for (int c = 0; c < C; ++c)
+      for (int b = 0; b < Bn; ++b) rt.push_back(make_int2(c, b));
+    std::stable_sort(rt.begin(), rt.end(), [](const int2& x, const int2& y) {
+      const int kx = 3 * x.x + x.y, ky = 3 * y.x + y.y;
+      return kx != ky ? kx < ky : x.x < y.x;
+    });
+    const uint64_t P = (uint64_t)l.g.P;
+    const uint64_t lines = (uint64_t)n * (uint64_t)n;
+    if (upload(ctx, &l.rw_tasks, rt.data(), (int64_t)rt.size()) ||
+        upload(ctx, &l.rw_prange, pr.data(), (int64_t)pr.size()) ||
+        dalloc(ctx, &l.bcell, (int64_t)C * Bn * n * 32) || dalloc(ctx, &l.ccell, (int64_t)C * Bn * n * R) ||
+        dalloc(ctx, &l.rw_ctl, 4))
+      return -1;
+    GMG_CHECK(ctx, cudaMemset(l.bcell, 0, sizeof(double2) * (size_t)C * Bn * n * 32));
+    GMG_CHECK(ctx, cudaMemset(l.ccell, 0, sizeof(double2) * (size_t)C * Bn * n * R));
+    GMG_CHECK(ctx, cudaMemset(l.rw_ctl, 0, sizeof(int) * 4));
+    if (!make_map3(&l.rmaps.u, l.u, P, (uint64_t)n, (uint64_t)n, 40, (uint32_t)(R + 2)) ||
+        !make_map3(&l.rmaps.f, l.f, P, (uint64_t)n, (uint64_t)n, 32, (uint32_t)R) ||
+        !make_map(&l.rmaps.m, CU_TENSOR_MAP_DATA_TYPE_UINT32, l.imask, (uint64_t)l.Cm, lines, (uint64_t)l.Cm * 4, 4,
+                  (uint32_t)R))
+      return fail(ctx, "gs_rows tensor maps failed");
+    l.rw_ntasks = (int)rt.size();
+    l.rw_C = C;
+    l.rw_Bn = Bn;
+    l.rows_gs = true;
+  }
 
   // coarsest direct-solve ordering: internal then ghost (ref operators.py:180)
   if (li == ctx->nlevels - 1) {

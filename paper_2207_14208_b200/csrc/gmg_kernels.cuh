@@ -57,6 +57,30 @@ struct BandArgs {
   double *v0, *v1;        // [nb + nfix] ping-pong values
 };
 
+#ifndef GS_ROWS
+#define GS_ROWS 4  // gs_rows.cu: grid rows per task (one compute warp each)
+#endif
+
+// gs_rows.cu: one grid row per warp, per-node cells between tasks
+struct GsRowArgs {
+  Geom g;
+  double* u;
+  const int2* tasks;    // (chunk c, block b), every task after (c-1, b) and (c, b-1)
+  const int2* prange;   // per task c * Bn + b: first / last plane with an internal node (first > last: none)
+  int ntasks, C, Bn;
+  int* ctl;             // [0] sweep sequence, [1] finished CTAs, [2] ticket (zero between sweeps)
+  double2* bcell;       // [c * Bn + b][N + 1][32]: (value, tag) of the block's last row, per plane
+  double2* ccell;       // [c * Bn + b][N + 1][GS_ROWS]: (value, tag) of the chunk's last column
+};
+struct RowMaps {
+  CUtensorMap u;  // (P, n, n) doubles, box 40 x (GS_ROWS + 2) x 1
+  CUtensorMap f;  // (P, n, n) doubles, box 32 x GS_ROWS x 1
+  CUtensorMap m;  // internal-node mask words (Cm, n * n), box 4 x GS_ROWS
+};
+void launch_gs_rows(const GsRowArgs& a, const RowMaps& maps, int grid, cudaStream_t st);
+size_t gs_rows_smem();
+int gs_rows_rows();
+
 void launch_gs_sweep(const GsArgs& a, int grid, cudaStream_t st);
 void launch_gs_stream(const GsArgs& a, int grid, int warps_per_cta, cudaStream_t st);
 size_t gs_stream_smem_per_warp();

@@ -99,20 +99,80 @@ def per_op_digests(ref, S, level, plan, coarse_plan, seed):
     return out
 
 
-def make_case(name, setup, cycles, seeds=(7,), rho=True, store_plan=True, coarse_solver="direct", norm="inf"):
+class MixedBCShim:
+    """SURVEY.md Appendix B mixed-BC shim over the REFERENCE's own functions:
+    the reference supports one BC kind per problem (operators.py:73-96,
+    smoothing.py:50-77), so per ghost the Dirichlet or Neumann row and dtau
+    are selected by ``selector(Q)`` from the reference's two single-kind
+    results.  Patched where the reference looks them up: SweepPlan
+    (smoothing.py:104), assemble_system for the coarsest matrix
+    (operators.py:208) and MultigridSolver.__init__ (solver.py:110)."""
+
+    def __init__(self, selector):
+        import ghostmg.operators as O
+        import ghostmg.smoothing as S
+        import ghostmg.solver as V
+        self.mods = (O, S, V)
+        self.orig_rows = O.ghost_row_weights
+        self.orig_dtau = S.assign_dtau
+        rows0, dtau0 = self.orig_rows, self.orig_dtau
+
+        def rows(cls, bc):
+            dm = np.asarray(selector(cls.ghost_Q), dtype=bool)
+            return np.where(dm[:, None], rows0(cls, "dirichlet"), rows0(cls, "neumann"))
+
+        def dtau(cls, bc, config, default_variant="poly"):
+            dm = np.asarray(selector(cls.ghost_Q), dtype=bool)
+            return np.where(dm, dtau0(cls, "dirichlet", config, default_variant),
+                            dtau0(cls, "neumann", config, default_variant))
+
+        self.rows, self.dtau = rows, dtau
+
+    def __enter__(self):
+        O, S, V = self.mods
+        O.ghost_row_weights = S.ghost_row_weights = self.rows
+        S.assign_dtau = V.assign_dtau = self.dtau
+        return self
+
+    def __exit__(self, *exc):
+        O, S, V = self.mods
+        O.ghost_row_weights = S.ghost_row_weights = self.orig_rows
+        S.assign_dtau = V.assign_dtau = self.orig_dtau
+
+
+def make_case(name, setup, cycles, seeds=(7,), rho=True, store_plan=True, coarse_solver="direct", norm="inf",
+              op_levels=None):
     sys.path.insert(0, "/root/reference/pkg/src")
+    import contextlib
+
     import ghostmg
     from ghostmg import smoothing as S
+    from ghostmg.geometry import compute_normal
     from ghostmg.smoothing import SmootherConfig as RSC
     from ghostmg.solver import CycleConfig as RCC
     from ghostmg.solver import build_solver, measure_rho
     from ghostmg.operators import ProblemSpec as RPS
 
     sp = setup.spec
-    rspec = RPS(sp.pde, sp.bc, sp.f, sp.g_box, sp.g_gamma)
+    mixed = sp.bc == "mixed"
+    # mixed BC: the reference is built as a Dirichlet problem with the
+    # per-ghost rows / dtau / coarsest matrix patched in, and g set directly
+    # (as tests/test_solver.py:95-97 of the reference does)
+    rspec = RPS(sp.pde, "dirichlet" if mixed else sp.bc, sp.f, sp.g_box, None if mixed else sp.g_gamma)
     cyc = RCC(scheme=setup.cycle.scheme, cycles=cycles, norm=norm, coarse_solver=coarse_solver)
-    ref = build_solver(ghostmg.UniformGrid(setup.grid.d, setup.grid.N), setup.phi, rspec,
-                       setup.faces, RSC(), cyc, setup.default_variant, setup.coarsest_min)
+    shim = MixedBCShim(sp.bc_selector) if mixed else contextlib.nullcontext()
+    with shim:
+        ref = build_solver(ghostmg.UniformGrid(setup.grid.d, setup.grid.N), setup.phi, rspec,
+                           setup.faces, RSC(), cyc, setup.default_variant, setup.coarsest_min)
+        if mixed:
+            ref._coarsest_matrix()  # factor the coarsest matrix with the mixed rows
+    if mixed:
+        cls = ref.levels[0].cls
+        dm = np.asarray(sp.bc_selector(cls.ghost_Q), dtype=bool)
+        normals = compute_normal(cls.phi, cls.ghost_Q, cls.grid.h)
+        g = np.asarray(sp.g_gamma(cls.ghost_Q, dm, normals), dtype=float).copy()
+        g[cls.ghost_promoted] = 0.0
+        ref.g_fine = g
     d = setup.grid.d
     if setup.f_seed is not None:
         f = uniform_symmetric(setup.f_seed, setup.grid.n_nodes) * setup.f_scale
@@ -127,6 +187,8 @@ def make_case(name, setup, cycles, seeds=(7,), rho=True, store_plan=True, coarse
                                        for k, v in p.to_arrays().items()})
     for seed in seeds:
         for lvl, p in enumerate(plans):
+            if op_levels is not None and lvl not in op_levels:
+                continue
             coarse = plans[lvl + 1] if lvl + 1 < len(plans) else None
             record["ops"][f"{seed}:{lvl}"] = per_op_digests(ref, S, lvl, p, coarse, seed)
     homogeneous = sp.f is None and setup.f_seed is None

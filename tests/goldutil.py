@@ -52,6 +52,32 @@ def plans(name):
     return load_plans(os.path.join(GOLDEN, f"{name}.npz"))
 
 
+def rebuild(name):
+    """(plans, extra) of a golden case rebuilt with the REPO's own host setup
+    (build_hierarchy + build_level_plan), for the cases too large to store
+    plans; test_setup_golden.py checks them against the reference's
+    plan_digests.  extra holds f_fine / g_fine / eliminated_values as the
+    reference's MultigridSolver would (pore space: the seeded f)."""
+    from paper_2207_14208_b200 import configs as CF
+    from paper_2207_14208_b200.cycle import CycleConfig, CycleDriver
+    from paper_2207_14208_b200.transfer import build_hierarchy
+
+    rec = record(name)
+    setup = CASES[name]["setup"]()
+    cyc = CycleConfig(scheme=rec["scheme"], cycles=rec["cycles"], norm=rec["norm"],
+                      coarse_solver=rec["coarse_solver"])
+    levels = build_hierarchy(setup.grid, setup.phi, setup.faces, max_levels=cyc.max_levels,
+                             coarsest_min=setup.coarsest_min)
+    plans, f, g, e = CycleDriver.problem_data(levels, setup.spec, setup.smoother, setup.default_variant)
+    if setup.f_seed is not None:
+        f = CF.pore_rhs(setup, plans[0].labels)
+    return plans, {"f_fine": f, "g_fine": g, "eliminated_values": e}
+
+
+def plans_or_rebuild(name):
+    return plans(name) if has_plans(name) else rebuild(name)
+
+
 def case_names(with_plans=None):
     names = sorted(os.path.basename(p)[:-5] for p in glob.glob(os.path.join(GOLDEN, "*.json"))
                    if not os.path.basename(p).startswith("_"))
@@ -123,6 +149,17 @@ def _cases():
                                                  ProblemSpec("poisson", "dirichlet"), "w", cmin=16),
                              cycles=16, store_plan=False),
         "pores64": dict(setup=lambda: CF.config_pores(N=64, cycles=15), cycles=15, store_plan=False),
+        # BASELINE configs at (or towards) their stated sizes, run by the reference
+        # itself; too large to store plans, so tests rebuild them with the repo's
+        # own setup, which must hash like the reference's (plan_digests)
+        "ball256": dict(setup=lambda: CF.config_ball(256), cycles=15, store_plan=False),        # c3
+        "flowerD2048": dict(setup=lambda: CF.config_flower_dirichlet(2048), cycles=20,          # c2 proxy
+                            store_plan=False),
+        "flowerM128": dict(setup=lambda: CF.config_flower(128), cycles=20),                     # c2 mixed BC
+        "flowerM256": dict(setup=lambda: CF.config_flower(256), cycles=20, store_plan=False),
+        "flowerM2048": dict(setup=lambda: CF.config_flower(2048), cycles=20, store_plan=False,  # c2 as specified
+                            rho=False),
+        "pores128": dict(setup=lambda: CF.config_pores(N=128, cycles=15), cycles=15, store_plan=False),
     }
     return cases
 

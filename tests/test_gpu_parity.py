@@ -16,7 +16,9 @@ from paper_2207_14208_b200.smoothing import SmootherConfig
 from paper_2207_14208_b200.solver import MultigridSolver
 
 pytestmark = pytest.mark.gpu
-PLAN_CASES = GU.case_names(with_plans=True)
+# every reference-golden case: stored plans, or rebuilt with the repo's setup
+# (tests/test_setup_golden.py pins those to the reference's plan digests)
+PLAN_CASES = GU.case_names()
 
 
 def device_op_digests(ctx, plans, level, seed):
@@ -78,7 +80,7 @@ def device_op_digests(ctx, plans, level, seed):
 @pytest.mark.parametrize("name", PLAN_CASES)
 def test_device_ops_match_reference(name, gpu_available):
     rec = GU.record(name)
-    plans, _ = GU.plans(name)
+    plans, _ = GU.plans_or_rebuild(name)
     ctx = _lib.Context(plans[0].d, len(plans))
     for i, p in enumerate(plans):
         ctx.set_level(i, p)
@@ -94,7 +96,7 @@ def test_device_ops_match_reference(name, gpu_available):
 
 def device_solver(name):
     rec = GU.record(name)
-    plans, extra = GU.plans(name)
+    plans, extra = GU.plans_or_rebuild(name)
     cyc = CycleConfig(scheme=rec["scheme"], cycles=rec["cycles"], norm=rec["norm"],
                       coarse_solver=rec["coarse_solver"])
     return rec, MultigridSolver.from_plans(plans, extra["f_fine"], extra["g_fine"],

@@ -15,7 +15,8 @@ from oracle.solver import OracleSolver
 from paper_2207_14208_b200.cycle import CycleConfig, measure_rho
 from paper_2207_14208_b200.smoothing import SmootherConfig
 
-PLAN_CASES = GU.case_names(with_plans=True)
+LARGE = {"ball256", "flowerD2048", "flowerM2048", "pores128"}
+CASES = [pytest.param(n, marks=pytest.mark.slow) if n in LARGE else n for n in GU.case_names()]
 
 
 def oracle_op_digests(plans, level, seed):
@@ -43,10 +44,10 @@ def oracle_op_digests(plans, level, seed):
     return out
 
 
-@pytest.mark.parametrize("name", PLAN_CASES)
+@pytest.mark.parametrize("name", CASES)
 def test_oracle_ops_match_reference(name):
     rec = GU.record(name)
-    plans, _ = GU.plans(name)
+    plans, _ = GU.plans_or_rebuild(name)
     for key, want in rec["ops"].items():
         seed, level = map(int, key.split(":"))
         got = oracle_op_digests(plans, level, seed)
@@ -55,14 +56,14 @@ def test_oracle_ops_match_reference(name):
 
 def oracle_from_golden(name):
     rec = GU.record(name)
-    plans, extra = GU.plans(name)
+    plans, extra = GU.plans_or_rebuild(name)
     cyc = CycleConfig(scheme=rec["scheme"], cycles=rec["cycles"], norm=rec["norm"],
                       coarse_solver=rec["coarse_solver"])
     return rec, OracleSolver(plans, extra["f_fine"], extra["g_fine"], extra["eliminated_values"],
                              SmootherConfig(), cyc)
 
 
-@pytest.mark.parametrize("name", PLAN_CASES)
+@pytest.mark.parametrize("name", CASES)
 def test_oracle_solve_matches_reference(name):
     rec, solver = oracle_from_golden(name)
     u0 = None if rec["solve"].get("from_initial_field") else np.zeros(solver.plans[0].n_nodes)
@@ -102,3 +103,13 @@ def test_ddot_model_matches_this_hosts_blas():
             x = rng.standard_normal(n) * np.exp(rng.uniform(-5, 5, n))
             y = rng.standard_normal(n)
             assert ops.ddot(x, y) == x @ y
+
+
+@pytest.mark.gpu
+def test_ddot_model_matches_gpu_box_blas():
+    """re-probe the OpenBLAS ddot tree on the GPU box's host
+    CPU (OpenBLAS picks its kernel by core, DYNAMIC_ARCH).  The kernels and
+    fixtures follow the build container's SkylakeX tree; a different tree
+    on the GPU host would make a reference run THERE round differently
+    (fixtures made here stay valid)."""
+    test_ddot_model_matches_this_hosts_blas()
