@@ -31,7 +31,7 @@ def needs_build():
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(verbose=False, force=False, csrc=CSRC, lib=LIB):
+def build(verbose=False, force=False, csrc=CSRC, lib=LIB, defines=()):
     """Compile `csrc` into `lib` (an alternate source tree / output path is
     for A/B experiments with tools/build_alt.sh)."""
     if not force and lib == LIB and not needs_build():
@@ -43,7 +43,7 @@ def build(verbose=False, force=False, csrc=CSRC, lib=LIB):
     procs = []
     for src in SOURCES:
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(csrc, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(csrc, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -94,6 +94,7 @@ struct DevLevel {
   int rw_ntasks = 0, rw_C = 0, rw_Bn = 0;
   double2 *bcell = nullptr, *ccell = nullptr;
   int* rw_ctl = nullptr;
+  long long* rw_hint = nullptr;
   RowMaps rmaps;
   // coarsest direct solve
   int64_t n_int = 0;
@@ -166,7 +167,7 @@ struct gmg_ctx {
   bool ghost_batched = false;
   bool gs_trace = false;       // record the GS task timeline (GMG_GS_TRACE=1)
   int gs_grid_cap = 0;         // > 0: at most this many GS CTAs (tests the multi-task loop)
-  int gs_rows = 1;             // 3-D levels N >= 64: gs_rows.cu (GMG_GS_ROWS=0: gs_macro.cu, same results)
+  int gs_rows = 0;             // 3-D levels N >= 64: gs_rows.cu with GMG_GS_ROWS=1 (same results; not yet faster)
   int64_t band_coop_max = 200000;  // band extensions up to this many nodes: one cooperative launch (GMG_BAND_COOP;
                                    // 128^3 49 -> 40 us, 64^3 47 -> 30 us; 256^3 (533 k nodes) was slower)
   int halo_multi = -1;         // GS halo loader: -1 by level size, 0 two-batch, 1 multi-batch (GMG_GS_HALO)
@@ -271,7 +272,7 @@ void free_level(DevLevel& l) {
                   l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off,
                   l.bfixpos, l.bnbr, l.bv0, l.bv1, l.gwl, l.gbasel, l.gnodel, l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g,
                   l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part, l.nd_crow, l.nd_ccol, l.nd_cval,
-                  l.rw_tasks, l.rw_prange, l.bcell, l.ccell, l.rw_ctl};  // ticket lives in progress
+                  l.rw_tasks, l.rw_prange, l.bcell, l.ccell, l.rw_ctl, l.rw_hint};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -469,6 +470,19 @@ bool make_map3(CUtensorMap* m, void* base, uint64_t cols, uint64_t rows, uint64_
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D tiled tensor map (cols fastest) with a box of box0 x box1 x box2 elements
+bool make_map3t(CUtensorMap* m, CUtensorMapDataType t, int esize, void* base, uint64_t cols, uint64_t rows,
+                uint64_t planes, uint32_t box0, uint32_t box1, uint32_t box2) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {cols, rows, planes};
+  cuuint64_t strides[2] = {cols * esize, cols * rows * esize};
+  cuuint32_t box[3] = {box0, box1, box2};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, t, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap* m, CUtensorMapDataType t, void* base, uint64_t cols, uint64_t rows,
               uint64_t pitch_bytes, uint32_t box0, uint32_t box1) {
   EncodeTiledFn fn = encode_fn();
@@ -505,6 +519,14 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
     r.ctl = l.rw_ctl;
     r.bcell = l.bcell;
     r.ccell = l.ccell;
+    r.hint = l.rw_hint;
+    r.trace = nullptr;
+    if (ctx->gs_trace) {
+      const int64_t tn = (int64_t)l.rw_ntasks * 24 + 8 * 8 * 1024;  // + per-step clocks of the first 8 tasks
+      if (!l.trace && dalloc(ctx, &l.trace, tn)) return -1;
+      GMG_CHECK(ctx, cudaMemsetAsync(l.trace, 0, sizeof(long long) * (size_t)tn, ctx->stream));
+      r.trace = l.trace;
+    }
     launch_gs_rows(r, l.rmaps, gs_cap(ctx, std::min(l.rw_ntasks, ctx->sms)), ctx->stream);
     ctx->launches++;
     return 0;
@@ -1392,15 +1414,19 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     if (upload(ctx, &l.rw_tasks, rt.data(), (int64_t)rt.size()) ||
         upload(ctx, &l.rw_prange, pr.data(), (int64_t)pr.size()) ||
         dalloc(ctx, &l.bcell, (int64_t)C * Bn * n * 32) || dalloc(ctx, &l.ccell, (int64_t)C * Bn * n * R) ||
-        dalloc(ctx, &l.rw_ctl, 4))
+        dalloc(ctx, &l.rw_ctl, 4) || dalloc(ctx, &l.rw_hint, (int64_t)C * Bn * 16))
       return -1;
+    GMG_CHECK(ctx, cudaMemset(l.rw_hint, 0, sizeof(long long) * (size_t)C * Bn * 16));
     GMG_CHECK(ctx, cudaMemset(l.bcell, 0, sizeof(double2) * (size_t)C * Bn * n * 32));
     GMG_CHECK(ctx, cudaMemset(l.ccell, 0, sizeof(double2) * (size_t)C * Bn * n * R));
     GMG_CHECK(ctx, cudaMemset(l.rw_ctl, 0, sizeof(int) * 4));
-    if (!make_map3(&l.rmaps.u, l.u, P, (uint64_t)n, (uint64_t)n, 40, (uint32_t)(R + 2)) ||
-        !make_map3(&l.rmaps.f, l.f, P, (uint64_t)n, (uint64_t)n, 32, (uint32_t)R) ||
-        !make_map(&l.rmaps.m, CU_TENSOR_MAP_DATA_TYPE_UINT32, l.imask, (uint64_t)l.Cm, lines, (uint64_t)l.Cm * 4, 4,
-                  (uint32_t)R))
+    const uint32_t G = (uint32_t)gs_rows_group();
+    (void)lines;
+    if (!make_map3t(&l.rmaps.u, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, l.u, P, (uint64_t)n, (uint64_t)n, 40,
+                    (uint32_t)(R + 2), G) ||
+        !make_map3t(&l.rmaps.f, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, l.f, P, (uint64_t)n, (uint64_t)n, 32, (uint32_t)R, G) ||
+        !make_map3t(&l.rmaps.m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, l.imask, (uint64_t)l.Cm, (uint64_t)n, (uint64_t)n, 4,
+                    (uint32_t)R, G))
       return fail(ctx, "gs_rows tensor maps failed");
     l.rw_ntasks = (int)rt.size();
     l.rw_C = C;
@@ -1888,7 +1914,7 @@ int64_t gmg_debug_gs_trace(gmg_ctx* ctx, int li, long long* host, int64_t cap) {
   if (li < 0 || li >= ctx->nlevels) return fail(ctx, "bad level");
   DevLevel& l = ctx->L[li];
   if (!l.trace) return 0;
-  const int64_t n = std::min<int64_t>(cap, (int64_t)l.ntasks * 24);
+  const int64_t n = std::min<int64_t>(cap, l.rows_gs ? (int64_t)l.rw_ntasks * 16 + 8 * 8 * 1024 : (int64_t)l.ntasks * 24);
   cudaSetDevice(ctx->device);
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   GMG_CHECK(ctx, cudaMemcpy(host, l.trace, sizeof(long long) * n, cudaMemcpyDeviceToHost));

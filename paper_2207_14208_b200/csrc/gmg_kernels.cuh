@@ -71,15 +71,18 @@ struct GsRowArgs {
   int* ctl;             // [0] sweep sequence, [1] finished CTAs, [2] ticket (zero between sweeps)
   double2* bcell;       // [c * Bn + b][N + 1][32]: (value, tag) of the block's last row, per plane
   double2* ccell;       // [c * Bn + b][N + 1][GS_ROWS]: (value, tag) of the chunk's last column
+  long long* hint;      // [c * Bn + b][16]: progress hint (sweep << 32 | plane), one 128-byte line per task
+  long long* trace;     // diagnostics: [ntasks][16] per task (ticket order), or null
 };
-struct RowMaps {
-  CUtensorMap u;  // (P, n, n) doubles, box 40 x (GS_ROWS + 2) x 1
-  CUtensorMap f;  // (P, n, n) doubles, box 32 x GS_ROWS x 1
-  CUtensorMap m;  // internal-node mask words (Cm, n * n), box 4 x GS_ROWS
+struct RowMaps {  // boxes of gs_rows_group() planes
+  CUtensorMap u;  // (P, n, n) doubles, box 40 x (GS_ROWS + 2) x G
+  CUtensorMap f;  // (P, n, n) doubles, box 32 x GS_ROWS x G
+  CUtensorMap m;  // internal-node mask words (Cm, n, n), box 4 x GS_ROWS x G
 };
 void launch_gs_rows(const GsRowArgs& a, const RowMaps& maps, int grid, cudaStream_t st);
 size_t gs_rows_smem();
 int gs_rows_rows();
+int gs_rows_group();
 
 void launch_gs_sweep(const GsArgs& a, int grid, cudaStream_t st);
 void launch_gs_stream(const GsArgs& a, int grid, int warps_per_cta, cudaStream_t st);
