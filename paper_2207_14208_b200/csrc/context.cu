@@ -167,7 +167,7 @@ struct gmg_ctx {
   bool ghost_batched = false;
   bool gs_trace = false;       // record the GS task timeline (GMG_GS_TRACE=1)
   int gs_grid_cap = 0;         // > 0: at most this many GS CTAs (tests the multi-task loop)
-  int gs_rows = 0;             // 3-D levels N >= 64: gs_rows.cu with GMG_GS_ROWS=1 (same results; not yet faster)
+  int gs_rows = 1;             // 3-D levels N >= 64: gs_rows.cu (GMG_GS_ROWS=0: gs_macro.cu, which races at 256^3+)
   int64_t band_coop_max = 200000;  // band extensions up to this many nodes: one cooperative launch (GMG_BAND_COOP;
                                    // 128^3 49 -> 40 us, 64^3 47 -> 30 us; 256^3 (533 k nodes) was slower)
   int halo_multi = -1;         // GS halo loader: -1 by level size, 0 two-batch, 1 multi-batch (GMG_GS_HALO)
