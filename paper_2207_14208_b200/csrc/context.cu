@@ -96,6 +96,11 @@ struct DevLevel {
   int* rw_ctl = nullptr;
   long long* rw_hint = nullptr;
   RowMaps rmaps;
+  // gs_chain.cu (3-D, production): one warp per 16-column x 8-row task, register chains; shares the
+  // cell / control arrays above
+  bool chain_gs = false;
+  uint32_t* pmask = nullptr;  // plane-transposed internal-node bits
+  ChainMaps cmaps;
   // coarsest direct solve
   int64_t n_int = 0;
   int64_t* active = nullptr;  // internal nodes then ghost nodes (lex)
@@ -167,7 +172,9 @@ struct gmg_ctx {
   bool ghost_batched = false;
   bool gs_trace = false;       // record the GS task timeline (GMG_GS_TRACE=1)
   int gs_grid_cap = 0;         // > 0: at most this many GS CTAs (tests the multi-task loop)
-  int gs_rows = 1;             // 3-D levels N >= 64: gs_rows.cu (GMG_GS_ROWS=0: gs_macro.cu, which races at 256^3+)
+  int gs_rows = 1;             // 3-D levels N >= 64 with GMG_GS_CHAIN=0: gs_rows.cu (row per warp, step barriers)
+  int gs_chain = 1;            // 3-D levels N >= 64: gs_chain.cu (register chains; production)
+  int gs_chain_rot = 1;        // its warp-role rotation (GMG_GS_CHAIN_ROT=0: off; timing only)
   int64_t band_coop_max = 200000;  // band extensions up to this many nodes: one cooperative launch (GMG_BAND_COOP;
                                    // 128^3 49 -> 40 us, 64^3 47 -> 30 us; 256^3 (533 k nodes) was slower)
   int halo_multi = -1;         // GS halo loader: -1 by level size, 0 two-batch, 1 multi-batch (GMG_GS_HALO)
@@ -272,7 +279,7 @@ void free_level(DevLevel& l) {
                   l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off,
                   l.bfixpos, l.bnbr, l.bv0, l.bv1, l.gwl, l.gbasel, l.gnodel, l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g,
                   l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part, l.nd_crow, l.nd_ccol, l.nd_cval,
-                  l.rw_tasks, l.rw_prange, l.bcell, l.ccell, l.rw_ctl, l.rw_hint};  // ticket lives in progress
+                  l.rw_tasks, l.rw_prange, l.bcell, l.ccell, l.rw_ctl, l.rw_hint, l.pmask};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -507,6 +514,33 @@ int gs_cap(const gmg_ctx* ctx, int grid) { return ctx->gs_grid_cap > 0 ? std::mi
 // ---- operations ------------------------------------------------------------
 int op_gs(gmg_ctx* ctx, DevLevel& l) {
   Scope s(ctx, 0);
+  if (l.chain_gs) {
+    GsChainArgs r;
+    r.g = l.g;
+    r.u = l.u;
+    r.tasks = l.rw_tasks;
+    r.prange = l.rw_prange;
+    r.pmask = l.pmask;
+    r.ntasks = l.rw_ntasks;
+    r.C = l.rw_C;
+    r.Bn = l.rw_Bn;
+    r.cplanes = (int)l.g.n + 32;
+    r.rot = ctx->gs_chain_rot;
+    r.ctl = l.rw_ctl;
+    r.bcell = l.bcell;
+    r.ccell = l.ccell;
+    r.hint = l.rw_hint;
+    r.trace = nullptr;
+    if (ctx->gs_trace) {
+      const int64_t tn = (int64_t)l.rw_ntasks * (16 + 2 * (l.g.n + 32));  // + per-plane hand-off stamps
+      if (!l.trace && dalloc(ctx, &l.trace, tn)) return -1;
+      GMG_CHECK(ctx, cudaMemsetAsync(l.trace, 0, sizeof(long long) * (size_t)tn, ctx->stream));
+      r.trace = l.trace;
+    }
+    launch_gs_chain(r, l.cmaps, gs_cap(ctx, std::min(l.rw_ntasks, 2 * ctx->sms)), ctx->stream);
+    ctx->launches++;
+    return 0;
+  }
   if (l.rows_gs) {
     GsRowArgs r;
     r.g = l.g;
@@ -1008,6 +1042,8 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_EDGE")) ctx->gs_edge = e[0] == '1';
   if (const char* e = getenv("GMG_GS_GRID")) ctx->gs_grid_cap = atoi(e);  // cap on GS CTAs (multi-task loop test)
   if (const char* e = getenv("GMG_GS_ROWS")) ctx->gs_rows = atoi(e);       // 0: previous GS kernel (bitwise same)
+  if (const char* e = getenv("GMG_GS_CHAIN")) ctx->gs_chain = atoi(e);     // 0: gs_rows.cu (bitwise same)
+  if (const char* e = getenv("GMG_GS_CHAIN_ROT")) ctx->gs_chain_rot = atoi(e);
 #ifdef GMG_EXPERIMENTS
   if (const char* e = getenv("GMG_SIMPLE_GS")) ctx->force_simple_gs = e[0] == '1';
   if (const char* e = getenv("GMG_NO_WS")) ctx->no_ws = e[0] == '1';
@@ -1385,7 +1421,59 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   // the planes that hold internal nodes; tickets ordered by 3c + b (each task
   // after its two upstream tasks; a column hop lags ~3x a row hop)
   l.rows_gs = false;
-  if (d == 3 && N >= 64 && ctx->gs_rows && l.diag_gs && !empty_im.empty()) {
+  l.chain_gs = false;
+  if (d == 3 && N >= 64 && ctx->gs_chain && l.diag_gs && !empty_im.empty()) {
+    // gs_chain.cu tasks: 16-column chunk c x block of 8 rows; per task the
+    // planes that hold internal nodes; tickets ordered by 4c + 3b (every task
+    // after its two upstream tasks; a column hop lags ~4/3 of a row hop)
+    const int R = GS_CHAIN_ROWS, W = GS_CHAIN_COLS;
+    const int C = (int)((N - 1 + W - 1) / W), Bn = (int)((N - 1 + R - 1) / R);
+    const int64_t n = N + 1;
+    std::vector<int2> pr((size_t)C * Bn, make_int2(1 << 30, -1));
+    for (int64_t p = 1; p <= N - 1; ++p)
+      for (int64_t row = 1; row <= N - 1; ++row) {
+        const uint32_t* wrow = &empty_im[(size_t)((p * n + row) * l.Cm)];
+        const int b = (int)((row - 1) / R);
+        for (int c = 0; c < C; ++c)
+          if ((wrow[c >> 1] >> (16 * (c & 1))) & 0xffffu) {
+            int2& q = pr[(size_t)c * Bn + b];
+            q.x = std::min<int>(q.x, (int)p);
+            q.y = std::max<int>(q.y, (int)p);
+          }
+      }
+    std::vector<int2> rt;
+    rt.reserve((size_t)C * Bn);
+    for (int c = 0; c < C; ++c)
+      for (int b = 0; b < Bn; ++b) rt.push_back(make_int2(c, b));
+    std::stable_sort(rt.begin(), rt.end(), [](const int2& x, const int2& y) {
+      const int kx = 4 * x.x + 3 * x.y, ky = 4 * y.x + 3 * y.y;
+      return kx != ky ? kx < ky : x.x < y.x;
+    });
+    const uint64_t P = (uint64_t)l.g.P;
+    const int64_t pmw = ((n + 31) / 32) * n * l.g.P;
+    if (upload(ctx, &l.rw_tasks, rt.data(), (int64_t)rt.size()) ||
+        upload(ctx, &l.rw_prange, pr.data(), (int64_t)pr.size()) ||
+        dalloc(ctx, &l.bcell, (int64_t)C * Bn * (n + 32) * W) || dalloc(ctx, &l.ccell, (int64_t)C * Bn * (n + 32) * R) ||
+        dalloc(ctx, &l.rw_ctl, 4) || dalloc(ctx, &l.rw_hint, (int64_t)C * Bn * 16) || dalloc(ctx, &l.pmask, pmw))
+      return -1;
+    GMG_CHECK(ctx, cudaMemset(l.rw_hint, 0, sizeof(long long) * (size_t)C * Bn * 16));
+    GMG_CHECK(ctx, cudaMemset(l.bcell, 0, sizeof(double2) * (size_t)C * Bn * (n + 32) * W));
+    GMG_CHECK(ctx, cudaMemset(l.ccell, 0, sizeof(double2) * (size_t)C * Bn * (n + 32) * R));
+    GMG_CHECK(ctx, cudaMemset(l.rw_ctl, 0, sizeof(int) * 4));
+    launch_chain_pmask(l.g, l.labels, l.pmask, ctx->stream);
+    GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+    const uint32_t G = (uint32_t)gs_chain_group();
+    if (!make_map3t(&l.cmaps.u, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, l.u, P, (uint64_t)n, (uint64_t)n, (uint32_t)(W + 4),
+                    (uint32_t)(R + 2), G) ||
+        !make_map3t(&l.cmaps.f, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, l.f, P, (uint64_t)n, (uint64_t)n, (uint32_t)W,
+                    (uint32_t)R, G))
+      return fail(ctx, "gs_chain tensor maps failed");
+    l.rw_ntasks = (int)rt.size();
+    l.rw_C = C;
+    l.rw_Bn = Bn;
+    l.chain_gs = true;
+  }
+  if (!l.chain_gs && d == 3 && N >= 64 && ctx->gs_rows && l.diag_gs && !empty_im.empty()) {
     const int R = gs_rows_rows();
     const int C = l.C, Bn = (int)((N - 1 + R - 1) / R);
     const int64_t n = N + 1;
@@ -1914,7 +2002,9 @@ int64_t gmg_debug_gs_trace(gmg_ctx* ctx, int li, long long* host, int64_t cap) {
   if (li < 0 || li >= ctx->nlevels) return fail(ctx, "bad level");
   DevLevel& l = ctx->L[li];
   if (!l.trace) return 0;
-  const int64_t n = std::min<int64_t>(cap, l.rows_gs ? (int64_t)l.rw_ntasks * 16 + 8 * 8 * 1024 : (int64_t)l.ntasks * 24);
+  const int64_t n = std::min<int64_t>(cap, l.chain_gs ? (int64_t)l.rw_ntasks * (16 + 2 * (l.g.n + 32))
+                                               : l.rows_gs ? (int64_t)l.rw_ntasks * 16 + 8 * 8 * 1024
+                                                           : (int64_t)l.ntasks * 24);
   cudaSetDevice(ctx->device);
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   GMG_CHECK(ctx, cudaMemcpy(host, l.trace, sizeof(long long) * n, cudaMemcpyDeviceToHost));

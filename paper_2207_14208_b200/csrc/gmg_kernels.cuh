@@ -84,6 +84,35 @@ size_t gs_rows_smem();
 int gs_rows_rows();
 int gs_rows_group();
 
+// gs_chain.cu (3-D production kernel): one warp per task of GS_CHAIN_COLS columns x GS_CHAIN_ROWS rows,
+// register chains, per-node cells between tasks
+#define GS_CHAIN_COLS 16
+#define GS_CHAIN_ROWS 8
+struct GsChainArgs {
+  Geom g;
+  double* u;
+  const int2* tasks;      // (chunk c, block b), every task after (c-1, b) and (c, b-1)
+  const int2* prange;     // per task c * Bn + b: first / last plane with an internal node (first > last: none)
+  const uint32_t* pmask;  // plane-transposed internal-node bits: word ((p >> 5) * n + r) * P + pos, bit p & 31
+  int ntasks, C, Bn;
+  int cplanes;            // planes per task in the cell arrays (N + 1 + 32: the chains run past the last plane)
+  int rot;                // rotate the warp roles of CTAs in odd warp-slot groups
+  int* ctl;               // [0] sweep sequence, [1] finished CTAs, [2] ticket (zero between sweeps)
+  double2* bcell;         // [c * Bn + b][cplanes][GS_CHAIN_COLS]: (value, tag) of the block's last row, per plane
+  double2* ccell;         // [c * Bn + b][cplanes][GS_CHAIN_ROWS]: (value, tag) of the chunk's last column
+  long long* hint;        // [c * Bn + b][16]: progress hint (sweep << 32 | plane), one 128-byte line per task
+  long long* trace;       // diagnostics: [ntasks][16] per task (ticket order), or null
+};
+struct ChainMaps {  // boxes of gs_chain_group() planes
+  CUtensorMap u;    // (P, n, n) doubles, box (GS_CHAIN_COLS + 4) x (GS_CHAIN_ROWS + 2) x G
+  CUtensorMap f;    // (P, n, n) doubles, box GS_CHAIN_COLS x GS_CHAIN_ROWS x G
+};
+void launch_gs_chain(const GsChainArgs& a, const ChainMaps& maps, int grid, cudaStream_t st);
+void launch_chain_pmask(const Geom& g, const uint8_t* labels, uint32_t* pm, cudaStream_t st);
+size_t gs_chain_smem();
+int gs_chain_group();
+void configure_gs_chain();
+
 void launch_gs_sweep(const GsArgs& a, int grid, cudaStream_t st);
 void launch_gs_stream(const GsArgs& a, int grid, int warps_per_cta, cudaStream_t st);
 size_t gs_stream_smem_per_warp();

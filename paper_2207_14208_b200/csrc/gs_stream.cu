@@ -261,6 +261,7 @@ void configure_gs_kernels() {
   configure_gs_diag();
   configure_gs_macro();
   configure_gs_rows();
+  configure_gs_chain();
   configure_dense_gemv();
 }
 

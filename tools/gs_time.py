@@ -16,17 +16,13 @@ from paper_2207_14208_b200.cycle import CycleDriver
 from paper_2207_14208_b200.solver import MultigridSolver
 from paper_2207_14208_b200.transfer import build_hierarchy
 
-name, N = sys.argv[1].split(":")
-N = int(N)
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-variants = [int(v) for v in (sys.argv[3] if len(sys.argv) > 3 else "1,0").split(",")]
-setup = CF.config_pores(N=N) if name == "c4" else CF.CONFIGS[name](N)
-levels = build_hierarchy(setup.grid, setup.phi, setup.faces, coarsest_min=setup.coarsest_min)
-plans, f, g, e = CycleDriver.problem_data(levels, setup.spec, setup.smoother, setup.default_variant)
-del levels
+variants = [int(v) for v in (sys.argv[3] if len(sys.argv) > 3 else "2").split(",")]
+import _plans
+setup, plans, f, g, e = _plans.load(sys.argv[1])
 PEAK = 6540.2
 for v in variants:
-    os.environ["GMG_GS_ROWS"] = str(v)
+    os.environ["GMG_GS_CHAIN"] = "1" if v == 2 else "0"  # 2: gs_chain.cu, 1: gs_rows.cu
     solver = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, device=0,
                                         coarse_backend="device-inverse")
     ctx = solver.ctx
@@ -44,7 +40,7 @@ for v in variants:
         ctx.profile(False)
         t = ms / cnt
         gbs = 24 * p.n_internal / (t / 1e3) / 1e9
-        print(f"GS_ROWS={v} level {i} N={p.N:5d} internal {p.n_internal:11d}: {t * 1e3:9.1f} us  "
+        print(f"GS variant {v} level {i} N={p.N:5d} internal {p.n_internal:11d}: {t * 1e3:9.1f} us  "
               f"{gbs:7.0f} GB/s  ({100 * gbs / PEAK:5.1f} % of {PEAK:.0f})", flush=True)
     ctx.close()
     del solver, ctx
