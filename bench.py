@@ -4,8 +4,8 @@ multigrid V-cycle on BASELINE.json config 4 (3D pore space, 512^3).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 One step = one V(2,1) cycle on the finest level plus the residual-norm
-record the reference's ``solve`` makes after every cycle
-(/root/reference/pkg/src/ghostmg/solver.py:224-232).  DOF = internal +
+record and the max|u| renormalisation guard the reference's ``solve`` makes
+after every cycle (/root/reference/pkg/src/ghostmg/solver.py:224-243).  DOF = internal +
 ghost unknowns of the finest level (the size of the linear system,
 operators.py:180).  Inputs (u, f) are HBM-resident when the timed region
 starts; every array is > L2 (1.08 GB per grid vector at 513^3), so no L2
@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--N", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-bitexact", action="store_true",
+                    help="skip the second timing with the host SuperLU coarsest solve (the bit-exact path)")
     ap.add_argument("--cpu-sample-cycles", type=int, default=1)
     ap.add_argument("--coarse", default="device-inverse", choices=["superlu", "device-inverse"],
                     help="coarsest solve: host SciPy SuperLU (bit-exact) or device dense inverse")
@@ -193,7 +195,8 @@ def run_reference(args, rank):
     s._put_u(np.zeros(plans[0].n_nodes))
     s._coarsest()
     # bounded sample: at most one warm-up cycle and as many of the K timed
-    # cycles as fit in ~150 s of host time (each full-size cycle is ~13 s)
+    # cycles as fit in ~150 s of host time (each full-size cycle is ~13 s);
+    # "steps" in the line is the number of cycles actually timed
     for _ in range(min(args.warmup, 1)):
         s._run_cycle()
         s._residual_norm()
@@ -209,8 +212,8 @@ def run_reference(args, rank):
     value = dof * done / dt
     line = {
         "impl": "reference", "metric": "fine-grid DOF*V-cycles/s (fp64)", "value": value,
-        "unit": "DOF*cycles/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / done * 1e3, "higher_is_better": True, "scaling": "weak",
+        "unit": "DOF*cycles/s", "n_gpus": args.gpus, "steps": done, "steps_requested": args.steps,
+        "warmup": min(args.warmup, 1), "ms_per_step": dt / done * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": setup.name, "N": setup.grid.N, "levels": len(plans), "dof": dof,
                    "cycle": "V(2,1)", "parallelism": "cpu-1thread"},
@@ -239,8 +242,19 @@ def run_b200(args, rank, world, local_rank):
 
     setup, plans, f, g, e, setup_times = build_workload(args)
     t0 = time.time()
-    solver = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, device=local_rank,
-                                        coarse_backend=args.coarse)
+    sharded = False
+    if world > 1 and plans[0].d == 3:
+        # z-slab sharding of the one problem over the ranks (strong scaling): planes exchanged as
+        # device tensors over NCCL, residual norm MAX-all-reduced, small levels agglomerated on rank 0
+        from paper_2207_14208_b200.slabs import TorchGroup, slab_solver
+
+        solver = slab_solver(plans, f, g, e, setup.smoother, setup.cycle, TorchGroup(dist, local_rank),
+                             device=local_rank, coarse_backend=args.coarse)
+        sharded = solver.part.distributed(0)
+    else:
+        solver = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, device=local_rank,
+                                            coarse_backend=args.coarse)
+    copies = 1 if sharded else world  # unsharded ranks are independent replicas of the whole problem
     log(f"[bench] upload + coarse factor {time.time() - t0:.1f}s, device bytes "
         f"{solver.ctx.device_bytes / 1e9:.2f} GB")
     ctx = solver.ctx
@@ -254,9 +268,15 @@ def run_b200(args, rank, world, local_rank):
 
     solver._set_data(f, g)
     solver._put_u(np.zeros(p0.n_nodes))
+    def step(s):
+        # what solve() does per cycle (reference solver.py:224-243): the cycle,
+        # the residual-norm record and the max|u| renormalisation guard
+        s._run_cycle()
+        s._residual_norm()
+        s._abs_max_scale()
+
     for _ in range(args.warmup):
-        solver._run_cycle()
-        solver._residual_norm()
+        step(solver)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -267,8 +287,7 @@ def run_b200(args, rank, world, local_rank):
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            solver._run_cycle()
-            solver._residual_norm()
+            step(solver)
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
@@ -278,8 +297,7 @@ def run_b200(args, rank, world, local_rank):
     # launches and CUDA events around every kernel class (same stream).
     ctx.profile(True)
     for _ in range(args.steps):
-        solver._run_cycle()
-        solver._residual_norm()
+        step(solver)
     gs_ms, gs_n = ctx.profile_read("gs_sweep", 0)
     breakdown = {}
     for k in _lib.KCLASS:
@@ -290,14 +308,18 @@ def run_b200(args, rank, world, local_rank):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = dof * args.steps * world / (ms / 1e3)
+    value = dof * args.steps * copies / (ms / 1e3)
 
     # roofline of the dominant kernel (fine-level GS sweep)
     peak, peak_kind = measured_peak()
     gs_bytes = 24 * p0.n_internal
+    if sharded:  # this rank's share of the sweep (internal nodes taken as uniform over the planes)
+        lo_, hi_ = solver.part.planes(0, rank)
+        gs_bytes = int(gs_bytes * (hi_ - lo_) / (p0.N + 1))
     gs_avg_s = gs_ms / max(gs_n, 1) / 1e3
     achieved = gs_bytes / gs_avg_s / 1e9 if gs_n else None
-    roofline = {"bound": "hbm", "kernel": "gs_macro_kernel (finest level GS-LEX sweep, 3-D two-chain)" if not os.environ.get("GMG_GS_MACRO", "1") == "0" else "gs_diag_kernel<3> (finest level GS-LEX sweep)",
+    roofline = {"bound": "hbm", "kernel": ("gs_chain_kernel" if p0.d == 3 and p0.N >= 64 else "gs_diag_kernel" if p0.N >= 64 else "gs_stream_kernel")
+                + " (finest level GS-LEX sweep)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(),
                 "algorithmic_bytes_per_launch": gs_bytes, "avg_launch_ms": gs_avg_s * 1e3,
@@ -319,17 +341,57 @@ def run_b200(args, rank, world, local_rank):
         u_out, rep = solver.solve(u=pin_u, cycles=args.steps)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
+        ran = max(rep.cycles_run, 1)  # solve() stops early at the divergence guard
         h2d = 8 * (2 * p0.n_nodes + p0.n_ghosts)
-        d2h = 8 * p0.n_nodes + 16 * (args.steps + 1)
-        e2e = {"value": dof * args.steps * world / dt, "unit": "DOF*cycles/s",
-               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-               "solve_s": dt, "cycles": args.steps, "final_residual": rep.residual_norms[-1],
+        d2h = 8 * p0.n_nodes + 24 * (ran + 1)
+        e2e = {"value": dof * rep.cycles_run * copies / dt, "unit": "DOF*cycles/s",
+               "h2d_bytes_per_step": h2d // ran, "d2h_bytes_per_step": d2h // ran,
+               "solve_s": dt, "cycles": rep.cycles_run, "cycles_requested": args.steps, "diverged": rep.diverged,
+               "final_residual": rep.residual_norms[-1],
                # convergence factor of this solve: geometric mean of the per-cycle
                # residual ratios after the first cycle (the reference's rho is the
                # mean ratio over cycles 11-15 of a 16-cycle measure_rho run)
                "conv_factor": (rep.residual_norms[-1] / rep.residual_norms[1]) ** (1.0 / (len(rep.residual_norms) - 2))
                if len(rep.residual_norms) > 2 and rep.residual_norms[1] > 0 else None,
                "rho_sequence": [float(x) for x in rep.rho_sequence]}
+
+    # parity at the bench size: the e2e solve's residual history against the C
+    # oracle's (tests/golden/_oracle_c4_512.json, zero initial guess; the oracle
+    # is pinned bit for bit to reference-run fixtures)
+    parity = None
+    fixture = os.path.join(ROOT, "tests", "golden", "_oracle_c4_512.json")
+    if e2e is not None and args.config == "c4" and setup.grid.N == 512 and os.path.exists(fixture):
+        with open(fixture) as fh:
+            want = [float.fromhex(x) for x in json.load(fh)["solve"]["residual_norms"]]
+        m = min(len(want), len(rep.residual_norms))
+        rel = [abs(a - b) / b for a, b in zip(rep.residual_norms[:m], want[:m])]
+        parity = {"against": "C oracle residual history at this size (tests/golden/_oracle_c4_512.json)",
+                  "cycles_compared": m - 1, "max_rel_diff": max(rel), "bitwise": rel == [0.0] * m,
+                  "coarse": args.coarse}
+
+    # the bit-exact path (host SciPy SuperLU coarsest solve through the callback)
+    bitexact = None
+    if not args.no_bitexact and args.coarse != "superlu" and setup.cycle.coarse_solver != "sweeps" and not sharded:
+        s2 = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, device=local_rank,
+                                        coarse_backend="superlu")
+        s2.ctx.set_stream(stream.cuda_stream)
+        s2._set_data(f, g)
+        s2._put_u(np.zeros(p0.n_nodes))
+        for _ in range(args.warmup):
+            step(s2)
+        torch.cuda.synchronize()
+        b0 = torch.cuda.Event(enable_timing=True)
+        b1 = torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(args.steps):
+            step(s2)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bms = b0.elapsed_time(b1)
+        bitexact = {"value": dof * args.steps * copies / (bms / 1e3), "unit": "DOF*cycles/s",
+                    "ms_per_step": bms / args.steps, "coarse": "direct:superlu (host callback, bitwise the reference)"}
+        s2.ctx.close()
+        del s2
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -343,13 +405,15 @@ def run_b200(args, rank, world, local_rank):
         line = {
             "metric": "fine-grid DOF*V-cycles/s (fp64)", "value": value, "unit": "DOF*cycles/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": setup.name, "N": setup.grid.N, "levels": len(plans),
                        "dof": dof, "N_I": p0.n_internal, "N_G": p0.n_ghosts, "cycle": "V(2,1)",
-                       "coarse": f"{setup.cycle.coarse_solver}:{args.coarse}", "parallelism": f"replicas{world}",
+                       "coarse": f"{setup.cycle.coarse_solver}:{args.coarse}", "parallelism": (f"z-slabs{world} (one problem; whole-slab pipelined sweeps, NCCL plane exchange)" if sharded
+                                       else f"replicas{world} (independent copies, not decomposed)" if world > 1 else "single-gpu"),
                        "l2_flush": f"not needed: every grid vector ({8 * p0.n_nodes / 1e9:.2f} GB) exceeds L2"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity, "bitexact_path": bitexact,
+            "gpu_launches": launches,
             "clocks": clocks.summary(), "breakdown_ms_per_cycle": breakdown, "setup": setup_times,
         }
         print(json.dumps(line), flush=True)

@@ -55,9 +55,33 @@ enum gmg_op {
   GMG_OP_INTERP_ADD = 9,     /* ref transfer.py:149-151 + solver.py:198      */
   GMG_OP_ZERO_U = 10,
   GMG_OP_COARSE_SOLVE = 11,  /* ref solver.py:157-166 on the coarsest level */
-  GMG_OP_RES_RESTRICT = 12   /* 3-D: smoothing.py:111-118 fused into transfer.py:88-93,
+  GMG_OP_RES_RESTRICT = 12,  /* 3-D: smoothing.py:111-118 fused into transfer.py:88-93,
                                 U, F(l) -> F(l+1) without materialising R_INT */
+  /* z-slab schedule (paper_2207_14208_b200/slabs.py): the band extension of
+     transfer.py:241-252 phase by phase, so the slabs can exchange a halo plane
+     between phases, and the tail of a cycle on an agglomerated level */
+  GMG_OP_BAND_BFS_REXT = 13, /* BFS group `count` of the extension of GMG_R_EXT  */
+  GMG_OP_BAND_BFS_U = 14,    /* ... of GMG_U                                      */
+  GMG_OP_BAND_STEP_REXT = 15,/* one Jacobi transport step on GMG_R_EXT            */
+  GMG_OP_BAND_STEP_U = 16,   /* ... on GMG_U                                      */
+  GMG_OP_CYCLE_TAIL = 17     /* ref solver.py:190-197 from level l down: U(l) = 0, gamma cycles
+                                (or the coarsest solve) with F(l), G(l), then the band
+                                extension of U(l)                                 */
 };
+
+/* z-slab mode: this context updates only the planes
+ * [lo, hi) (reference axis 0, geometry.py:108-111) of level `level`: the GS
+ * and ghost sweeps (smoothing.py:127-142), both residuals and the norms
+ * (smoothing.py:111-124, solver.py:135-142) touch only nodes / ghosts of those
+ * planes; the other operations still run on the whole level, which is
+ * harmless because the slab schedule refreshes the neighbour planes they read.
+ * Only 3-D levels with N >= 64 can be split; lo = 0, hi = N + 1 restores the
+ * whole level.  Returns the number of BFS groups of the level's band plan. */
+int gmg_set_slab(gmg_ctx* ctx, int level, int64_t lo, int64_t hi);
+
+/* max |u| over the planes [lo, hi) of the finest level (the slab's part of the
+ * renormalisation guard, reference solver.py:239-243). */
+int gmg_abs_max_planes(gmg_ctx* ctx, int64_t lo, int64_t hi, double* peak);
 
 /* Library version (major*10000 + minor*100 + patch). */
 int gmg_version(void);

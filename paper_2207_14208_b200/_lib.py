@@ -19,6 +19,7 @@ OP_GS_SWEEP, OP_GHOST_SWEEP, OP_SMOOTH, OP_RES_INT, OP_RES_GHOST = 0, 1, 2, 3, 4
 OP_EXTEND_REXT, OP_EXTEND_U, OP_RESTRICT_INT, OP_RESTRICT_GHOST, OP_INTERP_ADD, OP_ZERO_U = 5, 6, 7, 8, 9, 10
 OP_COARSE_SOLVE = 11
 OP_RES_RESTRICT = 12
+OP_BAND_BFS_REXT, OP_BAND_BFS_U, OP_BAND_STEP_REXT, OP_BAND_STEP_U, OP_CYCLE_TAIL = 13, 14, 15, 16, 17
 KCLASS = {"gs_sweep": 0, "ghost_sweep": 1, "residual": 2, "band": 3, "restrict": 4,
           "interp": 5, "coarse": 6, "norm": 7}
 
@@ -38,6 +39,8 @@ SIGNATURES = {
     "gmg_set_stream": (_i, [_p, _p]),
     "gmg_set_level": (_i, [_p, _i, _i64, _d, _p, _i64, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p]),
     "gmg_set_cycle": (_i, [_p, _i, _i, _i, _i, _i, _i]),
+    "gmg_set_slab": (_i, [_p, _i, _i64, _i64]),
+    "gmg_abs_max_planes": (_i, [_p, _i64, _i64, _p]),
     "gmg_set_coarse_callback": (_i, [_p, COARSE_CB, _p]),
     "gmg_set_coarse_inverse": (_i, [_p, _i64, _p, _i]),
     "gmg_set_coarse_nd": (_i, [_p, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _i]),
@@ -152,6 +155,19 @@ class Context:
 
     def set_cycle(self, nu1, nu2, gamma, coarse_mode, coarse_sweeps, norm):
         self.check(self.lib.gmg_set_cycle(self.ctx, nu1, nu2, gamma, coarse_mode, coarse_sweeps, norm))
+
+    def set_slab(self, level, lo, hi):
+        """z-slab mode: this context updates planes [lo, hi) of `level` only.
+        Returns the number of BFS groups of the level's band plan."""
+        rc = self.lib.gmg_set_slab(self.ctx, level, lo, hi)
+        if rc < 0:
+            self.check(rc)
+        return rc
+
+    def abs_max_planes(self, lo, hi):
+        peak = np.zeros(1)
+        self.check(self.lib.gmg_abs_max_planes(self.ctx, lo, hi, ptr(peak)))
+        return float(peak[0])
 
     def set_coarse_callback(self, fn):
         """fn(rhs ndarray) -> solution ndarray."""

@@ -135,6 +135,14 @@ struct DevLevel {
   int32_t* nd_ccol = nullptr;   // used instead of the dense G when set
   double* nd_cval = nullptr;
   PwTree l2i, l2g;  // l2 residual norm: internal nodes (lex order), ghosts (lex order)
+  // z-slab mode (gmg_set_slab): this context updates only the planes [slab_lo, slab_hi) of the level
+  bool slab = false;
+  int64_t slab_lo = 0, slab_hi = 0;
+  std::vector<int2> h_prange;         // host copy of the gs_chain task plane ranges (unclipped)
+  std::vector<int32_t> slot_plane;    // plane of every ghost slot (-1: padding)
+  std::vector<int32_t> lex_plane;     // plane of every ghost, lexicographic order (ascending)
+  std::vector<int64_t> sb_lo, sb_hi;  // per sweep batch: the slots of the slab's planes
+  int64_t lex_lo = 0, lex_hi = 0;     // the ghosts (lexicographic) of the slab's planes
   bool ready = false;
 };
 
@@ -617,6 +625,16 @@ int op_ghost_sweep(gmg_ctx* ctx, DevLevel& l) {
   Scope s(ctx, 1);
   GhostArgs a = ghost_args(l);
   const int nb = (int)l.batch_off.size() - 1;
+  if (l.slab) {
+    // z-slab mode: the slab's ghosts batch by batch (the batches are the levels of the sweep DAG, so
+    // launch order gives every ghost its predecessors' new values; those of other slabs are already in u)
+    for (int b = 0; b < nb; ++b)
+      if (l.sb_hi[b] > l.sb_lo[b]) {
+        launch_ghost_batch(a, l.u, l.sb_lo[b], l.sb_hi[b], nullptr, ctx->stream);
+        ctx->launches++;
+      }
+    return 0;
+  }
   if (ctx->ghost_batched) {  // one launch per batch (reference path for experiments)
     for (int b = 0; b < nb; ++b) {
       launch_ghost_batch(a, l.u, l.batch_off[b], l.batch_off[b + 1], nullptr, ctx->stream);
@@ -658,7 +676,12 @@ int op_smooth(gmg_ctx* ctx, DevLevel& l, int count) {
 int op_res_int(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
   Scope s(ctx, slot ? 7 : 2);
   // the norm pass (slot set) only needs the maximum: no residual array writes
-  launch_residual_interior(l.g, l.labels, l.u, l.f, slot ? nullptr : l.rI, slot, ctx->stream);
+  if (l.slab && l.g.d == 3)
+    launch_residual_interior_planes(l.g, l.labels, l.u, l.f, slot ? nullptr : l.rI, slot,
+                                    (int)std::max<int64_t>(1, l.slab_lo), (int)std::min<int64_t>(l.g.N - 1, l.slab_hi - 1),
+                                    ctx->stream);
+  else
+    launch_residual_interior(l.g, l.labels, l.u, l.f, slot ? nullptr : l.rI, slot, ctx->stream);
   ctx->launches++;
   return 0;
 }
@@ -666,9 +689,10 @@ int op_res_int(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
 int op_res_ghost(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
   if (l.ng == 0) return 0;
   Scope s(ctx, slot ? 7 : 2);
+  if (l.slab && l.lex_hi <= l.lex_lo) return 0;
   if (l.gwl)
     launch_residual_ghost_lex(ghost_args(l), l.gwl, l.gbasel, l.gnodel, l.lex2slot, l.ng, l.u, slot ? nullptr : l.rE,
-                              slot, ctx->stream);
+                              slot, l.slab ? l.lex_lo : 0, l.slab ? l.lex_hi : l.ng, ctx->stream);
   else
     launch_residual_ghost(ghost_args(l), l.u, slot ? nullptr : l.rE, slot, ctx->stream);
   ctx->launches++;
@@ -1230,6 +1254,15 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     lexmap.clear();
     lexmap.shrink_to_fit();
     if (dep.empty()) dep.push_back(0);
+    {
+      const int64_t per = d == 3 ? (N + 1) * (N + 1) : (N + 1);
+      l.slot_plane.assign((size_t)ns, -1);
+      l.lex_plane.resize((size_t)ng);
+      for (int64_t i = 0; i < ng; ++i) {
+        l.lex_plane[(size_t)i] = (int32_t)(ghost_idx[i] / per);
+        l.slot_plane[(size_t)l2s[i]] = l.lex_plane[(size_t)i];
+      }
+    }
     if (upload(ctx, &l.gnode, node.data(), ns) || upload(ctx, &l.gbase, base.data(), ns) ||
         upload(ctx, &l.gw, w.data(), (int64_t)m * ns) || upload(ctx, &l.gdtau, dt.data(), ns) ||
         upload(ctx, &l.gprom, pr.data(), ns) || upload(ctx, &l.slot2lex, s2l.data(), ns) ||
@@ -1451,6 +1484,7 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     });
     const uint64_t P = (uint64_t)l.g.P;
     const int64_t pmw = ((n + 31) / 32) * n * l.g.P;
+    l.h_prange = pr;
     if (upload(ctx, &l.rw_tasks, rt.data(), (int64_t)rt.size()) ||
         upload(ctx, &l.rw_prange, pr.data(), (int64_t)pr.size()) ||
         dalloc(ctx, &l.bcell, (int64_t)C * Bn * (n + 32) * W) || dalloc(ctx, &l.ccell, (int64_t)C * Bn * (n + 32) * R) ||
@@ -1545,6 +1579,66 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     launch_restrict_mask(fl.g, fl.labels, clv.g, clv.labels, clv.rmask, ctx->stream);
     GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   }
+  return 0;
+}
+
+int gmg_set_slab(gmg_ctx* ctx, int li, int64_t lo, int64_t hi) {
+  if (li < 0 || li >= ctx->nlevels || !ctx->L[li].ready) return fail(ctx, "level not set");
+  DevLevel& l = ctx->L[li];
+  const int64_t n = l.g.n;
+  if (lo < 0 || hi > n || lo >= hi) return fail(ctx, "bad plane range");
+  cudaSetDevice(ctx->device);
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  graph_reset(ctx);
+  const bool whole = lo == 0 && hi == n;
+  if (!whole && !l.chain_gs) return fail(ctx, "only 3-D levels with N >= 64 (gs_chain levels) can be split into slabs");
+  l.slab = !whole;
+  l.slab_lo = lo;
+  l.slab_hi = hi;
+  if (l.chain_gs) {
+    // the GS tasks' plane ranges clipped to the slab: planes outside are left alone (and their
+    // neighbours' values, refreshed by the schedule, are read from u like any other halo)
+    std::vector<int2> pr = l.h_prange;
+    for (auto& q : pr) {
+      q.x = std::max<int>(q.x, (int)lo);
+      q.y = std::min<int>(q.y, (int)hi - 1);
+      if (q.x > q.y) q = make_int2(1 << 30, -1);
+    }
+    GMG_CHECK(ctx, cudaMemcpy(l.rw_prange, pr.data(), sizeof(int2) * pr.size(), cudaMemcpyHostToDevice));
+  }
+  // the slab's ghosts: a contiguous range in lexicographic order, one contiguous range per sweep batch
+  auto lb = [&](const std::vector<int32_t>& v, int64_t a, int64_t b, int64_t plane) {
+    return (int64_t)(std::lower_bound(v.begin() + a, v.begin() + b, (int32_t)plane) - v.begin());
+  };
+  l.lex_lo = lb(l.lex_plane, 0, l.ng, lo);
+  l.lex_hi = lb(l.lex_plane, 0, l.ng, hi);
+  const int nb = (int)l.batch_off.size() - 1;
+  l.sb_lo.assign(std::max(nb, 0), 0);
+  l.sb_hi.assign(std::max(nb, 0), 0);
+  for (int b = 0; b < nb; ++b) {
+    // slots of a batch are in lexicographic order, padding (-1) at its end
+    int64_t a0 = l.batch_off[b], a1 = l.batch_off[b + 1];
+    while (a1 > a0 && l.slot_plane[(size_t)a1 - 1] < 0) --a1;
+    l.sb_lo[b] = lb(l.slot_plane, a0, a1, lo);
+    l.sb_hi[b] = lb(l.slot_plane, a0, a1, hi);
+  }
+  return (int)l.bfs_off.size() - 1;
+}
+
+int gmg_abs_max_planes(gmg_ctx* ctx, int64_t lo, int64_t hi, double* peak) {
+  cudaSetDevice(ctx->device);
+  DevLevel& l = ctx->L[0];
+  const int64_t per = l.g.d == 3 ? l.g.n * l.g.P : l.g.P;
+  if (lo < 0 || hi > l.g.n || lo > hi) return fail(ctx, "bad plane range");
+  GMG_CHECK(ctx, cudaMemsetAsync(ctx->dmax + 2, 0, sizeof(unsigned long long), ctx->stream));
+  if (hi > lo) {
+    launch_abs_max(l.u + lo * per, (hi - lo) * per, ctx->dmax + 2, ctx->stream);
+    ctx->launches++;
+  }
+  GMG_CHECK(ctx, cudaMemcpyAsync(ctx->hmax + 2, ctx->dmax + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  std::memcpy(peak, ctx->hmax + 2, sizeof(double));
   return 0;
 }
 
@@ -1837,6 +1931,34 @@ int gmg_apply(gmg_ctx* ctx, int li, int op, int count) {
     case GMG_OP_COARSE_SOLVE:
       if (li != ctx->nlevels - 1) return fail(ctx, "coarse solve runs on the coarsest level");
       rc = coarse_solve(ctx, li);
+      break;
+    case GMG_OP_BAND_BFS_REXT:
+    case GMG_OP_BAND_BFS_U:
+      if (count < 0 || count + 1 >= (int)l.bfs_off.size()) return fail(ctx, "no such BFS group");
+      if (l.nb) {
+        Scope s(ctx, 3);
+        launch_band_bfs(band_args(l), op == GMG_OP_BAND_BFS_U ? l.u : l.rE, l.bfs_off[count], l.bfs_off[count + 1],
+                        ctx->stream);
+        ctx->launches++;
+      }
+      break;
+    case GMG_OP_BAND_STEP_REXT:
+    case GMG_OP_BAND_STEP_U:
+      if (l.nb) {
+        Scope s(ctx, 3);
+        launch_band_step(band_args(l), op == GMG_OP_BAND_STEP_U ? l.u : l.rE, ctx->stream);
+        ctx->launches += 3;
+      }
+      break;
+    case GMG_OP_CYCLE_TAIL:
+      if (li == ctx->nlevels - 1) {
+        rc = coarse_solve(ctx, li);
+      } else {
+        GMG_CHECK(ctx, cudaMemsetAsync(l.u, 0, sizeof(double) * (size_t)l.g.nodes, ctx->stream));
+        for (int k = 0; k < ctx->gamma && !rc; ++k) rc = cycle_level(ctx, li);
+      }
+      ctx->cur_level = li;
+      if (!rc) rc = op_extend(ctx, l, l.u);
       break;
     default: return fail(ctx, "unknown op");
   }

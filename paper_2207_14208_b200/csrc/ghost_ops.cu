@@ -333,11 +333,11 @@ __global__ void __launch_bounds__(256) residual_ghost_lex_kernel(GhostArgs a, co
                                                                  const int32_t* __restrict__ l2s, int64_t ng,
                                                                  const double* __restrict__ u,
                                                                  double* __restrict__ r_ext,
-                                                                 unsigned long long* maxbits) {
+                                                                 unsigned long long* maxbits, int64_t i0, int64_t i1) {
   constexpr int M = D == 3 ? 27 : 9;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double am = 0.0;
-  if (i < ng) {
+  if (i < i1) {
     const int64_t base = basel[i];
     double p[M];
 #pragma unroll
@@ -351,13 +351,13 @@ __global__ void __launch_bounds__(256) residual_ghost_lex_kernel(GhostArgs a, co
 
 void launch_residual_ghost_lex(const GhostArgs& a, const double* wl, const int64_t* basel, const int64_t* nodel,
                                const int32_t* l2s, int64_t ng, const double* u, double* r_ext,
-                               unsigned long long* maxbits, cudaStream_t st) {
-  if (ng == 0) return;
-  const int64_t blocks = (ng + 255) / 256;
+                               unsigned long long* maxbits, int64_t i0, int64_t i1, cudaStream_t st) {
+  if (i1 <= i0) return;
+  const int64_t blocks = (i1 - i0 + 255) / 256;
   if (a.g.d == 3)
-    residual_ghost_lex_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(a, wl, basel, nodel, l2s, ng, u, r_ext, maxbits);
+    residual_ghost_lex_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(a, wl, basel, nodel, l2s, ng, u, r_ext, maxbits, i0, i1);
   else
-    residual_ghost_lex_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(a, wl, basel, nodel, l2s, ng, u, r_ext, maxbits);
+    residual_ghost_lex_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(a, wl, basel, nodel, l2s, ng, u, r_ext, maxbits, i0, i1);
 }
 
 // Full-weighting row entry e of a 3^D block, ((1*a)*b)*c.

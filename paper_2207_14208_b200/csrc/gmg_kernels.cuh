@@ -140,10 +140,14 @@ void launch_residual_ghost(const GhostArgs& a, const double* u, double* r_ext,
                            unsigned long long* maxbits, cudaStream_t st);
 void launch_residual_ghost_lex(const GhostArgs& a, const double* wl, const int64_t* basel, const int64_t* nodel,
                                const int32_t* l2s, int64_t ng, const double* u, double* r_ext,
-                               unsigned long long* maxbits, cudaStream_t st);
+                               unsigned long long* maxbits, int64_t i0, int64_t i1, cudaStream_t st);
 void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,
                               const double* f, double* r, unsigned long long* maxbits,
                               cudaStream_t st);
+// the same over the internal planes [p_lo, p_hi] only (3-D, z-slab mode)
+void launch_residual_interior_planes(const Geom& g, const uint8_t* labels, const double* u, const double* f, double* r,
+                                     unsigned long long* maxbits, int p_lo, int p_hi, cudaStream_t st);
+void launch_band_step(const BandArgs& a, double* x, cudaStream_t st);
 void launch_band_bfs(const BandArgs& a, double* x, int64_t lo, int64_t hi, cudaStream_t st);
 void launch_band_transport(const BandArgs& a, double* x, cudaStream_t st);
 bool launch_band_coop(const BandArgs& a, double* x, const int64_t* goff, int ngroups, cudaStream_t st);

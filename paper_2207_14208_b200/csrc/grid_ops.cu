@@ -206,13 +206,14 @@ __global__ void __launch_bounds__(RM_TJ * 32) residual_march3_kernel(Geom g, con
                                                                      const double* __restrict__ u,
                                                                      const double* __restrict__ f,
                                                                      double* __restrict__ r,
-                                                                     unsigned long long* maxbits) {
+                                                                     unsigned long long* maxbits, int p_lo, int p_hi) {
   extern __shared__ __align__(16) unsigned char rm_raw[];
   ResMarchSmem<RM_TJ, RM_S>& S = *reinterpret_cast<ResMarchSmem<RM_TJ, RM_S>*>(rm_raw);
   const int N = (int)g.N;
   const int k0 = 1 + (int)blockIdx.x * RM_TK, j0 = 1 + (int)blockIdx.y * RM_TJ;
-  const int per = (N - 1 + (int)gridDim.z - 1) / (int)gridDim.z;
-  const int ib = 1 + (int)blockIdx.z * per, ie = min(N - 1, ib + per - 1);
+  // the internal planes [p_lo, p_hi] (1 .. N-1, or a z-slab of them) in gridDim.z segments
+  const int per = (p_hi - p_lo + 1 + (int)gridDim.z - 1) / (int)gridDim.z;
+  const int ib = p_lo + (int)blockIdx.z * per, ie = min(p_hi, ib + per - 1);
   if (ib > ie) return;
   const int tid = threadIdx.x;
   // Copy descriptors: each plane is the same set of RM_NCP copies (u rows with
@@ -315,10 +316,37 @@ __global__ void __launch_bounds__(RM_TJ * 32) residual_march3_kernel(Geom g, con
   block_max_commit(am, maxbits);
 }
 
+static void launch_residual_march(const Geom& g, const uint8_t* labels, const double* u, const double* f, double* r,
+                                  unsigned long long* maxbits, int p_lo, int p_hi, cudaStream_t st);
+
+void launch_residual_interior_planes(const Geom& g, const uint8_t* labels, const double* u, const double* f, double* r,
+                                     unsigned long long* maxbits, int p_lo, int p_hi, cudaStream_t st) {
+  if (p_hi >= p_lo) launch_residual_march(g, labels, u, f, r, maxbits, p_lo, p_hi, st);
+}
+
 void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,
                               const double* f, double* r, unsigned long long* maxbits,
                               cudaStream_t st) {
   if (g.d == 3 && !getenv("GMG_RES_ROWS")) {
+    launch_residual_march(g, labels, u, f, r, maxbits, 1, (int)g.N - 1, st);
+  } else if (g.d == 3 && getenv("GMG_RES_STREAM")) {
+    dim3 grid((unsigned)((g.N - 1 + RT_K - 1) / RT_K), (unsigned)((g.N - 1 + RT_J - 1) / RT_J));
+    residual_stream3_kernel<<<grid, 256, 0, st>>>(g, labels, u, f, r, maxbits);
+  } else if (g.d == 3) {
+    const int64_t nrows = (g.N - 1) * (g.N - 1);
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 16));
+    if (r)
+      residual_rows3_kernel<true><<<blocks, 128, 0, st>>>(g, labels, u, f, r, maxbits);
+    else
+      residual_rows3_kernel<false><<<blocks, 128, 0, st>>>(g, labels, u, f, r, maxbits);
+  } else {
+    residual_interior_kernel<2><<<grid_for(g.nodes, 256), 256, 0, st>>>(g, labels, u, f, r, maxbits);
+  }
+}
+
+static void launch_residual_march(const Geom& g, const uint8_t* labels, const double* u, const double* f, double* r,
+                                  unsigned long long* maxbits, int p_lo, int p_hi, cudaStream_t st) {
+  {
     // 8-row x 64-column tiles; ring of 4 plane slots (5 CTAs per SM) on the
     // largest grids, 5 slots (4 CTAs per SM) below N = 512 (measured per level)
     static bool attr = false;
@@ -336,31 +364,20 @@ void launch_residual_interior(const Geom& g, const uint8_t* labels, const double
     const bool big = g.N >= 512;
     const int per_sm = big ? 5 : 4;
     const int64_t tk = (g.N - 1 + RM_TK - 1) / RM_TK, tj = (g.N - 1 + 8 - 1) / 8;
-    const int64_t segs = std::max<int64_t>(1, std::min<int64_t>((g.N - 1) / 4, 148 * per_sm / (tk * tj)));
+    const int64_t np = p_hi - p_lo + 1;
+    const int64_t segs = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, np / 4), 148 * per_sm / (tk * tj)));
     dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)segs);
     if (big) {
       if (r)
-        residual_march3_kernel<true, 8, 4><<<grid, 256, sizeof(ResMarchSmem<8, 4>), st>>>(g, labels, u, f, r, maxbits);
+        residual_march3_kernel<true, 8, 4><<<grid, 256, sizeof(ResMarchSmem<8, 4>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi);
       else
-        residual_march3_kernel<false, 8, 4><<<grid, 256, sizeof(ResMarchSmem<8, 4>), st>>>(g, labels, u, f, r, maxbits);
+        residual_march3_kernel<false, 8, 4><<<grid, 256, sizeof(ResMarchSmem<8, 4>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi);
     } else {
       if (r)
-        residual_march3_kernel<true, 8, 5><<<grid, 256, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits);
+        residual_march3_kernel<true, 8, 5><<<grid, 256, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi);
       else
-        residual_march3_kernel<false, 8, 5><<<grid, 256, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits);
+        residual_march3_kernel<false, 8, 5><<<grid, 256, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi);
     }
-  } else if (g.d == 3 && getenv("GMG_RES_STREAM")) {
-    dim3 grid((unsigned)((g.N - 1 + RT_K - 1) / RT_K), (unsigned)((g.N - 1 + RT_J - 1) / RT_J));
-    residual_stream3_kernel<<<grid, 256, 0, st>>>(g, labels, u, f, r, maxbits);
-  } else if (g.d == 3) {
-    const int64_t nrows = (g.N - 1) * (g.N - 1);
-    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 16));
-    if (r)
-      residual_rows3_kernel<true><<<blocks, 128, 0, st>>>(g, labels, u, f, r, maxbits);
-    else
-      residual_rows3_kernel<false><<<blocks, 128, 0, st>>>(g, labels, u, f, r, maxbits);
-  } else {
-    residual_interior_kernel<2><<<grid_for(g.nodes, 256), 256, 0, st>>>(g, labels, u, f, r, maxbits);
   }
 }
 
@@ -1004,6 +1021,20 @@ void launch_band_transport(const BandArgs& a, double* x, cudaStream_t st) {
       band_iter_kernel<2><<<blocks, 256, 0, st>>>(a, vin, vout);
   }
   band_scatter_kernel<<<blocks, 256, 0, st>>>(a, a.v0, x);  // six steps: result back in v0
+}
+
+// One Jacobi transport step on the grid vector itself (z-slab mode: the slabs exchange a halo plane
+// of x between steps): gather, one step v0 -> v1, scatter v1.
+void launch_band_step(const BandArgs& a, double* x, cudaStream_t st) {
+  if (a.nb == 0) return;
+  const unsigned blocks = (unsigned)((a.nb + 255) / 256);
+  const unsigned gblocks = (unsigned)((a.nb + a.nfix + 255) / 256);
+  band_gather_kernel<<<gblocks, 256, 0, st>>>(a, x);
+  if (a.g.d == 3)
+    band_iter_kernel<3><<<blocks, 256, 0, st>>>(a, a.v0, a.v1);
+  else
+    band_iter_kernel<2><<<blocks, 256, 0, st>>>(a, a.v0, a.v1);
+  band_scatter_kernel<<<blocks, 256, 0, st>>>(a, a.v1, x);
 }
 
 // The whole band extension of a small level in one cooperative launch: the

@@ -206,6 +206,13 @@ __device__ __forceinline__ void stg_if(double* ptr, double v, bool p) {
   asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}\n" ::"l"(ptr), "d"(v), "r"((unsigned)p)
                : "memory");
 }
+// bits of mask word w (planes 32 w .. 32 w + 31) that lie in the planes [P0, P1]: the chains carry a
+// node along unchanged wherever its bit is clear, which is how planes outside the task's range -- also
+// those of another z-slab, which do hold internal nodes -- stay untouched
+__device__ __forceinline__ uint32_t wclip(int w, int P0, int P1) {
+  const int lo = max(P0 - 32 * w, 0), hi = min(P1 - 32 * w, 31);
+  return lo > 31 || hi < 0 ? 0u : ((0xffffffffu >> (31 - hi)) & (0xffffffffu << lo));
+}
 __device__ __forceinline__ unsigned slot_of(int p) { return (unsigned)((p + PBIAS) % NS); }
 
 }  // namespace
@@ -308,10 +315,10 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
         for (int i = 0; i < CH; ++i) {
           const int row = min(rowbase + CH * h + i, N);
           mp[i] = a.pmask + (size_t)row * g.P + (k0 + j + OFF);
-          mA[i] = wbw >= 0 ? ldg_u32(mp[i] + (size_t)wbw * wstride) : 0u;
-          mB[i] = wbw + 1 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 1) * wstride) : 0u;
-          mC[i] = wbw + 2 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 2) * wstride) : 0u;
-          mD[i] = wbw + 3 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 3) * wstride) : 0u;
+          mA[i] = wbw >= 0 ? ldg_u32(mp[i] + (size_t)wbw * wstride) & wclip(wbw, P0, P1) : 0u;
+          mB[i] = wbw + 1 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 1) * wstride) & wclip(wbw + 1, P0, P1) : 0u;
+          mC[i] = wbw + 2 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 2) * wstride) & wclip(wbw + 2, P0, P1) : 0u;
+          mD[i] = wbw + 3 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 3) * wstride) & wclip(wbw + 3, P0, P1) : 0u;
         }
         int fl0;
         do {
@@ -361,7 +368,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
               mA[i] = mB[i];
               mB[i] = mC[i];
               mC[i] = mD[i];
-              mD[i] = wbw + 3 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 3) * wstride) : 0u;
+              mD[i] = wbw + 3 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 3) * wstride) & wclip(wbw + 3, P0, P1) : 0u;
             }
           }
           {  // readiness of the block's planes (chain 0 leads: planes p .. p + KB - 1, chain i lags i)

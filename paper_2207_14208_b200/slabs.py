@@ -44,7 +44,9 @@ class LevelSlabs:
 class SlabPartition:
     """Plane ownership of every level."""
 
-    def __init__(self, Ns, world, min_planes=4):
+    def __init__(self, Ns, world, min_planes=4, min_N=0):
+        """``min_N``: levels with fewer cells per axis are agglomerated (the
+        device backend splits only levels with N >= 64, gmg_set_slab)."""
         self.world = world
         self.levels = []
         N0 = Ns[0]
@@ -60,8 +62,8 @@ class SlabPartition:
                 else:
                     nb = [0] + [x // 2 for x in bounds[1:-1]] + [N + 1]
                     bounds = nb if min(np.diff(nb)) >= min_planes else None
-            if li == len(Ns) - 1:
-                bounds = None  # the coarsest solve runs on rank 0
+            if li == len(Ns) - 1 or N < min_N:
+                bounds = None  # the coarsest solve (and every level too small to split) runs on rank 0
             self.levels.append(LevelSlabs(N, list(bounds) if bounds is not None else None))
 
     def distributed(self, level):
@@ -252,3 +254,336 @@ class SlabCycle:
         t = torch.from_numpy(np.ascontiguousarray(e))
         self.dist.broadcast(t, 0)
         return t.numpy().copy()
+
+
+# ---------------------------------------------------------------------------
+# Device backend: one gmg context per rank (one GPU each), planes exchanged as
+# device tensors (NCCL over NVLink through torch.distributed, or queues between
+# rank threads of one process for the single-GPU test).
+# ---------------------------------------------------------------------------
+class _DevMem:
+    """CUDA array interface view of `count` doubles at a device address."""
+
+    def __init__(self, address, count):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(address), False),
+                                         "version": 2}
+
+
+def device_tensor(address, count, device):
+    import torch
+
+    return torch.as_tensor(_DevMem(address, count), device=torch.device("cuda", device))
+
+
+class TorchGroup:
+    """torch.distributed (NCCL) transport of device tensors."""
+
+    def __init__(self, dist, device):
+        import torch
+
+        self.dist = dist
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.torch = torch
+        self.device = device
+
+    def _sync(self):
+        if self.device is not None:  # None: CPU tensors (gloo, tests)
+            self.torch.cuda.current_stream(self.device).synchronize()
+
+    def send(self, t, dst):
+        self.dist.send(t, dst)
+        self._sync()
+
+    def recv(self, t, src):
+        self.dist.recv(t, src)
+        self._sync()
+
+    def broadcast(self, t, src):
+        self.dist.broadcast(t, src)
+        self._sync()
+
+    def all_max(self, values):
+        dev = self.torch.device("cuda", self.device) if self.device is not None else self.torch.device("cpu")
+        t = self.torch.tensor(list(values), dtype=self.torch.float64, device=dev)
+        # NaN propagates like numpy's max: compare the bit patterns of the non-negative values
+        bits = t.view(self.torch.int64)
+        self.dist.all_reduce(bits, op=self.dist.ReduceOp.MAX)
+        return [float(x) for x in bits.view(self.torch.float64).cpu()]
+
+
+class LocalGroup:
+    """`world` rank threads of one process on one GPU (tests): blocking queues
+    between every ordered pair of ranks, the same interface as TorchGroup."""
+
+    class Shared:
+        def __init__(self, world):
+            import queue
+            import threading
+
+            self.world = world
+            self.q = {(a, b): queue.Queue() for a in range(world) for b in range(world)}
+            self.barrier = threading.Barrier(world)
+            self.slots = [None] * world
+
+    def __init__(self, shared, rank, device=0):
+        import torch
+
+        self.sh = shared
+        self.rank = rank
+        self.world = shared.world
+        self.torch = torch
+        self.device = device
+
+    def send(self, t, dst):
+        c = t.clone()
+        self.torch.cuda.synchronize(self.device)
+        self.sh.q[(self.rank, dst)].put(c)
+
+    def recv(self, t, src):
+        c = self.sh.q[(src, self.rank)].get(timeout=600)
+        t.copy_(c)
+        self.torch.cuda.synchronize(self.device)
+
+    def broadcast(self, t, src):
+        if self.rank == src:
+            for r in range(self.world):
+                if r != src:
+                    self.send(t, r)
+        else:
+            self.recv(t, src)
+
+    def all_max(self, values):
+        self.sh.slots[self.rank] = np.array(list(values), dtype=np.float64)
+        self.sh.barrier.wait()
+        allv = np.stack(self.sh.slots)
+        bits = allv.view(np.int64).max(axis=0)
+        out = [float(x) for x in bits.view(np.float64)]
+        self.sh.barrier.wait()
+        return out
+
+
+class DeviceSlabCycle:
+    """SlabCycle's schedule over a device hierarchy (`_lib.Context`, every
+    level uploaded whole on every rank; distributed levels in z-slab mode,
+    see gmg_set_slab in include/ghostmg_b200.h).  Reference: solver.py:170-199;
+    the sweeps' rank order restates smoothing.py:127-142 across slabs."""
+
+    def __init__(self, ctx, plans, partition, group, nu1, nu2, gamma, halo_ghost=2):
+        from . import _lib
+
+        self.L = _lib
+        self.ctx = ctx
+        self.plans = plans
+        self.part = partition
+        self.grp = group
+        self.rank = group.rank
+        self.world = group.world
+        self.nu1, self.nu2, self.gamma = nu1, nu2, gamma
+        self.hg = halo_ghost
+        self.ngroups = {}
+        for lv, p in enumerate(plans):
+            if partition.distributed(lv):
+                lo, hi = partition.planes(lv, self.rank)
+                self.ngroups[lv] = ctx.set_slab(lv, lo, hi)
+
+    # ---- plane transport (device tensors over the padded device layout) ----
+    def _plane_elems(self, level):
+        p = self.plans[level]
+        n = p.N + 1
+        pitch = max((p.N + 4 + 3) // 4 * 4, 32 * ((p.N - 1 + 31) // 32) + 4)  # make_geom's row pitch
+        return (n if p.d == 3 else 1) * pitch
+
+    def _view(self, level, which, lo, hi):
+        per = self._plane_elems(level)
+        base = self.ctx.device_pointer(level, which)
+        return device_tensor(base + 8 * lo * per, (hi - lo) * per, self.grp.device)
+
+    def _send(self, level, which, lo, hi, dst):
+        if hi > lo:
+            self.grp.send(self._view(level, which, lo, hi), dst)
+
+    def _recv(self, level, which, lo, hi, src):
+        if hi > lo:
+            self.grp.recv(self._view(level, which, lo, hi), src)
+
+    def halo(self, level, which, width):
+        if not self.part.distributed(level) or self.world == 1:
+            return
+        lo, hi = self.part.planes(level, self.rank)
+        N = self.part.levels[level].N
+        r = self.rank
+        for phase in ((0, 1) if r % 2 == 0 else (1, 0)):
+            if phase == 0:
+                if r + 1 < self.world:
+                    self._send(level, which, max(lo, hi - width), hi, r + 1)
+                if r > 0:
+                    self._send(level, which, lo, min(hi, lo + width), r - 1)
+            else:
+                if r > 0:
+                    plo, _ = self.part.planes(level, r - 1)
+                    self._recv(level, which, max(plo, lo - width), lo, r - 1)
+                if r + 1 < self.world:
+                    _, nhi = self.part.planes(level, r + 1)
+                    self._recv(level, which, hi, min(nhi, hi + width, N + 1), r + 1)
+
+    def _pipelined(self, level, width, op):
+        if not self.part.distributed(level) or self.world == 1:
+            self.ctx.apply(level, op)
+            return
+        self.halo(level, self.L.U, width)  # old values on both sides
+        lo, hi = self.part.planes(level, self.rank)
+        if self.rank > 0:
+            plo, _ = self.part.planes(level, self.rank - 1)
+            self._recv(level, self.L.U, max(plo, lo - width), lo, self.rank - 1)
+        self.ctx.apply(level, op)
+        if self.rank + 1 < self.world:
+            self._send(level, self.L.U, max(lo, hi - width), hi, self.rank + 1)
+
+    # ---- operations ---------------------------------------------------------
+    def smooth(self, level, count):
+        for _ in range(count):
+            self._pipelined(level, 1, self.L.OP_GS_SWEEP)
+            self._pipelined(level, self.hg, self.L.OP_GHOST_SWEEP)
+
+    def extrapolate(self, level, which):
+        bfs = self.L.OP_BAND_BFS_U if which == self.L.U else self.L.OP_BAND_BFS_REXT
+        step = self.L.OP_BAND_STEP_U if which == self.L.U else self.L.OP_BAND_STEP_REXT
+        for grp in range(self.ngroups[level]):
+            self.halo(level, which, 1)
+            self.ctx.apply(level, bfs, grp)
+        for _ in range(6):
+            self.halo(level, which, 1)
+            self.ctx.apply(level, step)
+
+    def residual_norm(self):
+        self.halo(0, self.L.U, self.hg)
+        m_int, m_g = self.ctx.residual_parts(0)
+        return self.grp.all_max([m_int, m_g])
+
+    def cycle(self, level):
+        L = self.L
+        ctx = self.ctx
+        self.smooth(level, self.nu1)
+        self.halo(level, L.U, self.hg)
+        ctx.apply(level, L.OP_RES_INT)
+        ctx.apply(level, L.OP_RES_GHOST)
+        self.extrapolate(level, L.R_EXT)
+        self.halo(level, L.R_INT, 1)
+        self.halo(level, L.R_EXT, 1)
+        c = level + 1
+        ctx.apply(level, L.OP_RESTRICT_INT)
+        ctx.apply(level, L.OP_RESTRICT_GHOST)
+        if self.part.distributed(c):
+            ctx.apply(c, L.OP_ZERO_U)
+            for _ in range(self.gamma):
+                self.cycle(c)
+            self.extrapolate(c, L.U)
+            self.halo(c, L.U, 1)
+        else:
+            # the coarse planes I with 2I in this rank's fine slab are right here: collect them (and the
+            # right-hand sides of the coarse ghosts on them) on rank 0, which finishes the cycle alone
+            self._collect_coarse(level)
+            if self.rank == 0:
+                ctx.apply(c, L.OP_CYCLE_TAIL)
+            n = self.plans[c].N + 1
+            self.grp.broadcast(self._view(c, L.U, 0, n), 0)
+        ctx.apply(level, L.OP_INTERP_ADD)
+        self.smooth(level, self.nu2)
+
+    def _collect_coarse(self, level):
+        import torch
+
+        L = self.L
+        c = level + 1
+        pc = self.plans[c]
+        per = (pc.N + 1) ** (pc.d - 1)
+        ranges = []
+        for r in range(self.world):
+            lo, hi = self.part.planes(level, r)
+            ranges.append(((lo + 1) // 2, (hi + 1) // 2))
+        gplane = pc.ghost_idx // per  # ascending
+        if self.rank == 0:
+            g = self.ctx.get_vector(c, L.G, pc.n_ghosts) if pc.n_ghosts else np.zeros(0)
+            for r in range(1, self.world):
+                lo, hi = ranges[r]
+                self._recv(c, L.F, lo, hi, r)
+                a, b = np.searchsorted(gplane, [lo, hi])
+                if b > a:
+                    t = torch.empty(b - a, dtype=torch.float64, device=torch.device("cuda", self.grp.device))
+                    self.grp.recv(t, r)
+                    g[a:b] = t.cpu().numpy()
+            if pc.n_ghosts:
+                self.ctx.set_vector(c, L.G, g)
+        else:
+            lo, hi = ranges[self.rank]
+            self._send(c, L.F, lo, hi, 0)
+            a, b = np.searchsorted(gplane, [lo, hi])
+            if b > a:
+                g = self.ctx.get_vector(c, L.G, pc.n_ghosts)
+                self.grp.send(torch.from_numpy(g[a:b].copy()).to(torch.device("cuda", self.grp.device)), 0)
+
+    def gather_planes(self, level, which):
+        """Every rank's owned planes of a vector onto every rank."""
+        if not self.part.distributed(level) or self.world == 1:
+            return
+        for r in range(self.world):
+            lo, hi = self.part.planes(level, r)
+            self.grp.broadcast(self._view(level, which, lo, hi), r)
+
+
+def slab_solver(plans, f_fine, g_fine, eliminated_values, smoother, cycle, group, device=0,
+                coarse_backend="device-inverse", min_planes=4):
+    """A `MultigridSolver` whose cycles run z-slab sharded over the ranks of
+    `group` (TorchGroup / LocalGroup): same `solve` / `measure_rho` API
+    (reference solver.py:215-298), every rank returns the whole iterate."""
+    from . import _lib
+    from .solver import MultigridSolver
+
+    class SlabSolver(MultigridSolver):
+        def _init_slabs(self):
+            Ns = [p.N for p in self.plans]
+            if self.plans[0].d != 3:
+                raise ValueError("z-slab sharding is for 3-D hierarchies")
+            self.part = SlabPartition(Ns, group.world, min_planes=min_planes, min_N=64)
+            self.slabs = DeviceSlabCycle(self.ctx, self.plans, self.part, group, self.smoother.nu1, self.smoother.nu2,
+                                         self.cycle_cfg.gamma)
+            self.group = group
+
+        def _run_cycle(self):
+            if self.part.distributed(0):
+                self.slabs.cycle(0)
+            else:
+                self.ctx.cycle(1)
+
+        def _residual_norm(self):
+            if not self.part.distributed(0):
+                return MultigridSolver._residual_norm(self)
+            m_int, m_g = self.slabs.residual_norm()
+            p = self.plans[0]
+            m = m_int if p.n_internal else 0.0
+            return max(m, m_g) if p.n_ghosts else m
+
+        def _abs_max_scale(self):
+            if not self.part.distributed(0):
+                return MultigridSolver._abs_max_scale(self)
+            lo, hi = self.part.planes(0, group.rank)
+            peak = group.all_max([self.ctx.abs_max_planes(lo, hi)])[0]
+            scaled = 0.0 < peak < 1e-250
+            if scaled:
+                self.ctx.scale_u(1e250)
+                self.ctx.synchronize()
+            return peak, scaled
+
+        def _get_u(self):
+            self.slabs.gather_planes(0, _lib.U)
+            return MultigridSolver._get_u(self)
+
+        def _fetch_u(self, u):
+            self.slabs.gather_planes(0, _lib.U)
+            return MultigridSolver._fetch_u(self, u)
+
+    s = SlabSolver.from_plans(plans, f_fine, g_fine, eliminated_values, smoother, cycle, device=device,
+                              coarse_backend=coarse_backend)
+    s._init_slabs()
+    return s

@@ -218,3 +218,53 @@ def test_partition_shapes():
     p = SlabPartition([64, 32, 16, 8], 3)
     assert p.distributed(1) and not p.distributed(2)  # odd coarse boundary: agglomerated
     assert not SlabPartition([16, 8, 4], 8).distributed(0)  # too thin: single rank
+
+
+def _group_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2207_14208_b200.slabs import TorchGroup
+
+        grp = TorchGroup(dist, None)  # CPU tensors over gloo; on the GPUs the same calls run over NCCL
+        t = torch.full((5,), float(rank), dtype=torch.float64)
+        if rank == 0:
+            grp.send(t, 1)
+            grp.recv(t, 1)
+        else:
+            r = torch.empty(5, dtype=torch.float64)
+            grp.recv(r, 0)
+            grp.send(t, 0)
+            t = r
+        b = torch.full((3,), 7.0 + rank, dtype=torch.float64)
+        grp.broadcast(b, 1)
+        m = grp.all_max([1.0 + rank, float("nan") if rank == 1 else 0.5, 0.0])
+        q.put((rank, t.tolist(), b.tolist(), m))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torch_group_transport_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_group_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][0] == [1.0] * 5 and res[1][0] == [0.0] * 5  # the two ranks swapped their planes
+    assert res[0][1] == [8.0] * 3 and res[1][1] == [8.0] * 3   # broadcast from rank 1
+    for r in (0, 1):
+        m = res[r][2]
+        assert m[0] == 2.0 and np.isnan(m[1]) and m[2] == 0.0  # MAX with numpy's NaN propagation
+
+
+def test_partition_min_N_agglomerates_small_levels():
+    p = SlabPartition([512, 256, 128, 64, 32], 8, min_N=64)
+    assert [p.distributed(i) for i in range(5)] == [True, True, True, True, False]
+    p = SlabPartition([256, 128, 64, 32, 16], 4, min_N=64)
+    assert [p.distributed(i) for i in range(5)] == [True, True, True, False, False]
