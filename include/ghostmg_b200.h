@@ -83,6 +83,17 @@ int gmg_set_slab(gmg_ctx* ctx, int level, int64_t lo, int64_t hi);
  * renormalisation guard, reference solver.py:239-243). */
 int gmg_abs_max_planes(gmg_ctx* ctx, int64_t lo, int64_t hi, double* peak);
 
+/* The seeded initial iterate on the device (reference solver.py:205-213:
+ * uniform(-1, 1) from XorShift64Star(seed), rng.py:14-56, prescribed values on
+ * eliminated nodes, 0 on inactive ones) written straight into GMG_U of the
+ * finest level.  `state` is the seeded generator state, `jump_cols` holds K
+ * sets of 64 column images: set b is the GF(2) matrix of `lane_len * 2^b`
+ * generator steps (K * 64 words; K must cover the number of lanes).  The
+ * eliminated nodes come as (flat index, value) pairs.  Bit for bit the
+ * sequential stream of the reference. */
+int gmg_initial_field(gmg_ctx* ctx, uint64_t state, const uint64_t* jump_cols, int K, int64_t lane_len,
+                      int64_t n_elim, const int64_t* elim_idx, const double* elim_val);
+
 /* Library version (major*10000 + minor*100 + patch). */
 int gmg_version(void);
 

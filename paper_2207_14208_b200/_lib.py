@@ -41,6 +41,7 @@ SIGNATURES = {
     "gmg_set_cycle": (_i, [_p, _i, _i, _i, _i, _i, _i]),
     "gmg_set_slab": (_i, [_p, _i, _i64, _i64]),
     "gmg_abs_max_planes": (_i, [_p, _i64, _i64, _p]),
+    "gmg_initial_field": (_i, [_p, ctypes.c_uint64, _p, _i, _i64, _i64, _p, _p]),
     "gmg_set_coarse_callback": (_i, [_p, COARSE_CB, _p]),
     "gmg_set_coarse_inverse": (_i, [_p, _i64, _p, _i]),
     "gmg_set_coarse_nd": (_i, [_p, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _i]),
@@ -163,6 +164,22 @@ class Context:
         if rc < 0:
             self.check(rc)
         return rc
+
+    def initial_field(self, seed, n_nodes, elim_idx, elim_val, lane_len=64):
+        """Seeded initial iterate generated on the device (reference
+        solver.py:205-213) into U of the finest level."""
+        from . import rng
+
+        lanes = -(-int(n_nodes) // lane_len)
+        K = max(1, (lanes - 1).bit_length())
+        cols = [rng._power_columns(lane_len)]
+        for _ in range(K - 1):
+            cols.append(rng._compose(cols[-1], cols[-1]))
+        jc = np.array(cols, dtype=np.uint64).reshape(-1)
+        idx = np.ascontiguousarray(elim_idx, dtype=np.int64)
+        val = np.ascontiguousarray(elim_val, dtype=np.float64)
+        self.check(self.lib.gmg_initial_field(self.ctx, rng.seed_state(seed), ptr(jc), K, lane_len, len(idx),
+                                              ptr(idx), ptr(val)))
 
     def abs_max_planes(self, lo, hi):
         peak = np.zeros(1)

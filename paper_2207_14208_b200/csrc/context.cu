@@ -88,14 +88,12 @@ struct DevLevel {
   bool diag_gs = false;       // lane-diagonal ring kernel (production, N >= 64)
   WsMaps maps;                // its tensor maps (u, f, imask)
   int *progress = nullptr, *ticket = nullptr;
-  // gs_rows.cu (3-D, production): row-per-warp tasks, cells between tasks
-  bool rows_gs = false;
+  // gs_chain.cu (3-D, production) task data: cells between tasks, control words
   int2 *rw_tasks = nullptr, *rw_prange = nullptr;
   int rw_ntasks = 0, rw_C = 0, rw_Bn = 0;
   double2 *bcell = nullptr, *ccell = nullptr;
   int* rw_ctl = nullptr;
   long long* rw_hint = nullptr;
-  RowMaps rmaps;
   // gs_chain.cu (3-D, production): one warp per 16-column x 8-row task, register chains; shares the
   // cell / control arrays above
   bool chain_gs = false;
@@ -180,8 +178,8 @@ struct gmg_ctx {
   bool ghost_batched = false;
   bool gs_trace = false;       // record the GS task timeline (GMG_GS_TRACE=1)
   int gs_grid_cap = 0;         // > 0: at most this many GS CTAs (tests the multi-task loop)
-  int gs_rows = 1;             // 3-D levels N >= 64 with GMG_GS_CHAIN=0: gs_rows.cu (row per warp, step barriers)
-  int gs_chain = 1;            // 3-D levels N >= 64: gs_chain.cu (register chains; production)
+  int gs_chain = 1;            // 3-D levels N >= 64: gs_chain.cu (register chains; production); GMG_GS_CHAIN=0:
+                               // the lane-diagonal ring kernel gs_diag.cu (bitwise the same results)
   int gs_chain_rot = 1;        // its warp-role rotation (GMG_GS_CHAIN_ROT=0: off; timing only)
   int64_t band_coop_max = 200000;  // band extensions up to this many nodes: one cooperative launch (GMG_BAND_COOP;
                                    // 128^3 49 -> 40 us, 64^3 47 -> 30 us; 256^3 (533 k nodes) was slower)
@@ -193,11 +191,7 @@ struct gmg_ctx {
   int ghost_backoff = 300;     // ghost sweep: poll back-off ns (GMG_GHOST_BACKOFF)
   int gs_sleep[4] = {500, 500, 20, 200};  // GS loader / writer back-off (ns), GMG_GS_SLEEP=u,f,h,w  // one launch per ghost batch instead of the persistent sweep
   int ws_ctas_per_sm = 4;
-  int gs_macro = 1;            // 3-D GS: two line chains per lane (gs_macro.cu; GMG_GS_MACRO=0: gs_diag.cu)
-  bool gs_edge = false;        // gs_macro: per-cell row-above hand-off (GMG_GS_EDGE=1; measured slower)
   int gs_pstride = 32;         // ints between progress words: one 128-byte line per task (GMG_GS_PSTRIDE=4: 16 B)
-  int macro_ctas = 0;          // its CTAs per SM (GMG_GS_MACRO_CTAS; 0: by task count)
-  int macro_occ = 0;           // its resident CTAs per SM (occupancy query on first use)
   bool prof = false;
   int prof_mask = 0;   // bit k: time kernel class k
   int cur_level = -1;  // level tag for profiling records
@@ -549,30 +543,6 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
     ctx->launches++;
     return 0;
   }
-  if (l.rows_gs) {
-    GsRowArgs r;
-    r.g = l.g;
-    r.u = l.u;
-    r.tasks = l.rw_tasks;
-    r.prange = l.rw_prange;
-    r.ntasks = l.rw_ntasks;
-    r.C = l.rw_C;
-    r.Bn = l.rw_Bn;
-    r.ctl = l.rw_ctl;
-    r.bcell = l.bcell;
-    r.ccell = l.ccell;
-    r.hint = l.rw_hint;
-    r.trace = nullptr;
-    if (ctx->gs_trace) {
-      const int64_t tn = (int64_t)l.rw_ntasks * 24 + 8 * 8 * 1024;  // + per-step clocks of the first 8 tasks
-      if (!l.trace && dalloc(ctx, &l.trace, tn)) return -1;
-      GMG_CHECK(ctx, cudaMemsetAsync(l.trace, 0, sizeof(long long) * (size_t)tn, ctx->stream));
-      r.trace = l.trace;
-    }
-    launch_gs_rows(r, l.rmaps, gs_cap(ctx, std::min(l.rw_ntasks, ctx->sms)), ctx->stream);
-    ctx->launches++;
-    return 0;
-  }
   GMG_CHECK(ctx, cudaMemsetAsync(l.progress, 0, sizeof(int) * (size_t)(32 * l.C * l.Bn + 4), ctx->stream));
   GsArgs a;
   a.g = l.g;
@@ -585,8 +555,7 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
   a.ticket = l.ticket;
   a.progress = l.progress;
   a.pstride = ctx->gs_pstride;
-  // per-cell row-above hand-off (gs_macro)
-  a.edge = (ctx->gs_edge && ctx->gs_macro) ? l.edge : nullptr;
+  a.edge = nullptr;
   a.empty_cb = l.tempty_cb;
   a.B1 = l.B1;
   a.Bn = l.Bn;
@@ -601,16 +570,7 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
     GMG_CHECK(ctx, cudaMemsetAsync(l.trace, 0, sizeof(long long) * (size_t)l.ntasks * 24, ctx->stream));
     a.trace = l.trace;
   }
-  if (l.diag_gs && l.g.d == 3 && ctx->gs_macro) {
-    // CTAs per SM: all that fit once the tasks exceed twice the resident
-    // capacity (1024^3, 2368 tasks on 148 SMs x 3: 8.65 ms at three vs 8.96 at
-    // two), else two (512^3, 592 tasks: 1.34 vs 1.36 ms, within run-to-run
-    // noise; profiles/r01k_gs_ctas_ab.txt)
-    if (ctx->macro_occ <= 0) ctx->macro_occ = gs_macro_ctas_per_sm();
-    const int per_sm = ctx->macro_ctas > 0 ? ctx->macro_ctas
-                       : (a.ntasks > 2 * ctx->macro_occ * ctx->sms ? ctx->macro_occ : std::min(2, ctx->macro_occ));
-    launch_gs_macro(a, l.maps, gs_cap(ctx, std::min(a.ntasks, per_sm * ctx->sms)), ctx->stream);
-  } else if (l.diag_gs)
+  if (l.diag_gs)
     launch_gs_diag(a, l.maps, gs_cap(ctx, std::min(a.ntasks, ctx->ws_ctas_per_sm * ctx->sms)), ctx->stream);
   else if (l.stream_gs)
     launch_gs_stream(a, std::min(l.ntasks, 4 * ctx->sms), 1, ctx->stream);
@@ -1063,10 +1023,8 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   // arithmetic).  Timing experiments need a -DGMG_EXPERIMENTS build.
   if (const char* e = getenv("GMG_NO_GRAPH")) ctx->use_graph = e[0] != '1';
   if (const char* e = getenv("GMG_GS_TRACE")) ctx->gs_trace = e[0] == '1';
-  if (const char* e = getenv("GMG_GS_EDGE")) ctx->gs_edge = e[0] == '1';
   if (const char* e = getenv("GMG_GS_GRID")) ctx->gs_grid_cap = atoi(e);  // cap on GS CTAs (multi-task loop test)
-  if (const char* e = getenv("GMG_GS_ROWS")) ctx->gs_rows = atoi(e);       // 0: previous GS kernel (bitwise same)
-  if (const char* e = getenv("GMG_GS_CHAIN")) ctx->gs_chain = atoi(e);     // 0: gs_rows.cu (bitwise same)
+  if (const char* e = getenv("GMG_GS_CHAIN")) ctx->gs_chain = atoi(e);     // 0: gs_diag.cu (bitwise same)
   if (const char* e = getenv("GMG_GS_CHAIN_ROT")) ctx->gs_chain_rot = atoi(e);
 #ifdef GMG_EXPERIMENTS
   if (const char* e = getenv("GMG_SIMPLE_GS")) ctx->force_simple_gs = e[0] == '1';
@@ -1075,9 +1033,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_FUSE_RES")) ctx->fuse_res_restrict = e[0] == '1';
   if (const char* e = getenv("GMG_GHOST_BATCHED")) ctx->ghost_batched = e[0] == '1';
   if (const char* e = getenv("GMG_GS_HALO")) ctx->halo_multi = atoi(e);
-  if (const char* e = getenv("GMG_GS_MACRO")) ctx->gs_macro = atoi(e);
   if (const char* e = getenv("GMG_GS_PSTRIDE")) ctx->gs_pstride = atoi(e) >= 32 ? 32 : 4;
-  if (const char* e = getenv("GMG_GS_MACRO_CTAS")) ctx->macro_ctas = atoi(e);
   if (const char* e = getenv("GMG_BAND_COOP")) ctx->band_coop_max = atoll(e);
   if (const char* e = getenv("GMG_GHOST_BPS")) ctx->ghost_bps = std::max(1, atoi(e));
   if (const char* e = getenv("GMG_GHOST_RAW")) ctx->ghost_raw_only = e[0] != '0';
@@ -1439,21 +1395,12 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     if (l.edge) cudaFree(l.edge);
     l.edge = nullptr;
   }
-  if (l.diag_gs && d == 3 && ctx->gs_edge) {
-    const int64_t ne = (int64_t)l.C * l.Bn * (N + 1) * 64;
-    if (dalloc(ctx, &l.edge, ne)) return -1;
-    GMG_CHECK(ctx, cudaMemset(l.edge, 0, sizeof(double) * (size_t)ne));
-  }
   // progress words: 16 B per task (the TMA-store path writes them with bulk copies);
   // the older kernels use the first C * Bn ints
   if (upload(ctx, &l.tasks, tasks.data(), l.ntasks) || dalloc(ctx, &l.progress, 32 * l.C * l.Bn + 4))
     return -1;
   l.ticket = l.progress + 32 * l.C * l.Bn;
 
-  // gs_rows.cu tasks (3-D, N >= 64): chunk c x block of GS_ROWS rows; per task
-  // the planes that hold internal nodes; tickets ordered by 3c + b (each task
-  // after its two upstream tasks; a column hop lags ~3x a row hop)
-  l.rows_gs = false;
   l.chain_gs = false;
   if (d == 3 && N >= 64 && ctx->gs_chain && l.diag_gs && !empty_im.empty()) {
     // gs_chain.cu tasks: 16-column chunk c x block of 8 rows; per task the
@@ -1507,55 +1454,6 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     l.rw_Bn = Bn;
     l.chain_gs = true;
   }
-  if (!l.chain_gs && d == 3 && N >= 64 && ctx->gs_rows && l.diag_gs && !empty_im.empty()) {
-    const int R = gs_rows_rows();
-    const int C = l.C, Bn = (int)((N - 1 + R - 1) / R);
-    const int64_t n = N + 1;
-    std::vector<int2> pr((size_t)C * Bn, make_int2(1 << 30, -1));
-    for (int64_t p = 1; p <= N - 1; ++p)
-      for (int64_t row = 1; row <= N - 1; ++row) {
-        const uint32_t* wrow = &empty_im[(size_t)((p * n + row) * l.Cm)];
-        const int b = (int)((row - 1) / R);
-        for (int c = 0; c < C; ++c)
-          if (wrow[c]) {
-            int2& q = pr[(size_t)c * Bn + b];
-            q.x = std::min<int>(q.x, (int)p);
-            q.y = std::max<int>(q.y, (int)p);
-          }
-      }
-    std::vector<int2> rt;
-    rt.reserve((size_t)C * Bn);
-    for (int c = 0; c < C; ++c)
-      for (int b = 0; b < Bn; ++b) rt.push_back(make_int2(c, b));
-    std::stable_sort(rt.begin(), rt.end(), [](const int2& x, const int2& y) {
-      const int kx = 3 * x.x + x.y, ky = 3 * y.x + y.y;
-      return kx != ky ? kx < ky : x.x < y.x;
-    });
-    const uint64_t P = (uint64_t)l.g.P;
-    const uint64_t lines = (uint64_t)n * (uint64_t)n;
-    if (upload(ctx, &l.rw_tasks, rt.data(), (int64_t)rt.size()) ||
-        upload(ctx, &l.rw_prange, pr.data(), (int64_t)pr.size()) ||
-        dalloc(ctx, &l.bcell, (int64_t)C * Bn * n * 32) || dalloc(ctx, &l.ccell, (int64_t)C * Bn * n * R) ||
-        dalloc(ctx, &l.rw_ctl, 4) || dalloc(ctx, &l.rw_hint, (int64_t)C * Bn * 16))
-      return -1;
-    GMG_CHECK(ctx, cudaMemset(l.rw_hint, 0, sizeof(long long) * (size_t)C * Bn * 16));
-    GMG_CHECK(ctx, cudaMemset(l.bcell, 0, sizeof(double2) * (size_t)C * Bn * n * 32));
-    GMG_CHECK(ctx, cudaMemset(l.ccell, 0, sizeof(double2) * (size_t)C * Bn * n * R));
-    GMG_CHECK(ctx, cudaMemset(l.rw_ctl, 0, sizeof(int) * 4));
-    const uint32_t G = (uint32_t)gs_rows_group();
-    (void)lines;
-    if (!make_map3t(&l.rmaps.u, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, l.u, P, (uint64_t)n, (uint64_t)n, 40,
-                    (uint32_t)(R + 2), G) ||
-        !make_map3t(&l.rmaps.f, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, l.f, P, (uint64_t)n, (uint64_t)n, 32, (uint32_t)R, G) ||
-        !make_map3t(&l.rmaps.m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, l.imask, (uint64_t)l.Cm, (uint64_t)n, (uint64_t)n, 4,
-                    (uint32_t)R, G))
-      return fail(ctx, "gs_rows tensor maps failed");
-    l.rw_ntasks = (int)rt.size();
-    l.rw_C = C;
-    l.rw_Bn = Bn;
-    l.rows_gs = true;
-  }
-
   // coarsest direct-solve ordering: internal then ghost (ref operators.py:180)
   if (li == ctx->nlevels - 1) {
     std::vector<int64_t> act;
@@ -1623,6 +1521,45 @@ int gmg_set_slab(gmg_ctx* ctx, int li, int64_t lo, int64_t hi) {
     l.sb_hi[b] = lb(l.slot_plane, a0, a1, hi);
   }
   return (int)l.bfs_off.size() - 1;
+}
+
+int gmg_initial_field(gmg_ctx* ctx, uint64_t state, const uint64_t* jump_cols, int K, int64_t lane_len,
+                      int64_t n_elim, const int64_t* elim_idx, const double* elim_val) {
+  if (!ctx->L[0].ready) return fail(ctx, "level not set");
+  DevLevel& l = ctx->L[0];
+  const int64_t nflat = l.g.rows * l.g.n;
+  if (lane_len < 1 || K < 1 || K > 62) return fail(ctx, "bad lane layout");
+  const int64_t lanes = (nflat + lane_len - 1) / lane_len;
+  if ((lanes - 1) >> K) return fail(ctx, "jump matrices do not cover the lanes");
+  cudaSetDevice(ctx->device);
+  uint64_t* dcols = nullptr;
+  int64_t* didx = nullptr;
+  double* dval = nullptr;
+  int rc = 0;
+  if (upload(ctx, &dcols, jump_cols, (int64_t)64 * K)) return -1;
+  launch_initial_field(l.g, l.labels, l.u, state, dcols, K, lane_len, ctx->stream);
+  ctx->launches++;
+  if (n_elim > 0) {
+    std::vector<int64_t> pos((size_t)n_elim);
+    for (int64_t k = 0; k < n_elim; ++k) {
+      if (elim_idx[k] < 0 || elim_idx[k] >= nflat) rc = fail(ctx, "eliminated node out of range");
+      pos[(size_t)k] = flat_to_pos(l.g, elim_idx[k]);
+    }
+    if (!rc && (upload(ctx, &didx, pos.data(), n_elim) || upload(ctx, &dval, elim_val, n_elim))) rc = -1;
+    if (!rc) {
+      launch_scatter(didx, n_elim, dval, l.u, ctx->stream);
+      ctx->launches++;
+    }
+  }
+  cudaStreamSynchronize(ctx->stream);
+  const int64_t freed = 64 * K * 8 + (didx ? n_elim * 8 : 0) + (dval ? n_elim * 8 : 0);
+  if (dcols) cudaFree(dcols);
+  if (didx) cudaFree(didx);
+  if (dval) cudaFree(dval);
+  ctx->bytes -= freed;
+  if (rc) return rc;
+  GMG_CHECK(ctx, cudaGetLastError());
+  return 0;
 }
 
 int gmg_abs_max_planes(gmg_ctx* ctx, int64_t lo, int64_t hi, double* peak) {
@@ -2125,7 +2062,6 @@ int64_t gmg_debug_gs_trace(gmg_ctx* ctx, int li, long long* host, int64_t cap) {
   DevLevel& l = ctx->L[li];
   if (!l.trace) return 0;
   const int64_t n = std::min<int64_t>(cap, l.chain_gs ? (int64_t)l.rw_ntasks * (16 + 2 * (l.g.n + 32))
-                                               : l.rows_gs ? (int64_t)l.rw_ntasks * 16 + 8 * 8 * 1024
                                                            : (int64_t)l.ntasks * 24);
   cudaSetDevice(ctx->device);
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));

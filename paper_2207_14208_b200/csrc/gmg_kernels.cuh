@@ -57,33 +57,6 @@ struct BandArgs {
   double *v0, *v1;        // [nb + nfix] ping-pong values
 };
 
-#ifndef GS_ROWS
-#define GS_ROWS 4  // gs_rows.cu: grid rows per task (one compute warp each)
-#endif
-
-// gs_rows.cu: one grid row per warp, per-node cells between tasks
-struct GsRowArgs {
-  Geom g;
-  double* u;
-  const int2* tasks;    // (chunk c, block b), every task after (c-1, b) and (c, b-1)
-  const int2* prange;   // per task c * Bn + b: first / last plane with an internal node (first > last: none)
-  int ntasks, C, Bn;
-  int* ctl;             // [0] sweep sequence, [1] finished CTAs, [2] ticket (zero between sweeps)
-  double2* bcell;       // [c * Bn + b][N + 1][32]: (value, tag) of the block's last row, per plane
-  double2* ccell;       // [c * Bn + b][N + 1][GS_ROWS]: (value, tag) of the chunk's last column
-  long long* hint;      // [c * Bn + b][16]: progress hint (sweep << 32 | plane), one 128-byte line per task
-  long long* trace;     // diagnostics: [ntasks][16] per task (ticket order), or null
-};
-struct RowMaps {  // boxes of gs_rows_group() planes
-  CUtensorMap u;  // (P, n, n) doubles, box 40 x (GS_ROWS + 2) x G
-  CUtensorMap f;  // (P, n, n) doubles, box 32 x GS_ROWS x G
-  CUtensorMap m;  // internal-node mask words (Cm, n, n), box 4 x GS_ROWS x G
-};
-void launch_gs_rows(const GsRowArgs& a, const RowMaps& maps, int grid, cudaStream_t st);
-size_t gs_rows_smem();
-int gs_rows_rows();
-int gs_rows_group();
-
 // gs_chain.cu (3-D production kernel): one warp per task of GS_CHAIN_COLS columns x GS_CHAIN_ROWS rows,
 // register chains, per-node cells between tasks
 #define GS_CHAIN_COLS 16
@@ -124,8 +97,6 @@ struct WsMaps {
 };
 void launch_gs_diag(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st);
 size_t gs_diag_smem();
-void launch_gs_macro(const GsArgs& a, const WsMaps& maps, int grid, cudaStream_t st);
-int gs_macro_ctas_per_sm();
 void configure_gs_kernels();  // set max dynamic shared memory of the GS / GEMV kernels
 
 void launch_ghost_batch(const GhostArgs& a, double* u, int64_t lo, int64_t hi, double* pair, cudaStream_t st);
@@ -162,6 +133,8 @@ void launch_restrict_ghost(const Geom& gf, const uint8_t* lab_f, const double* r
                            cudaStream_t st);
 void launch_interp_add(const Geom& gf, const uint8_t* lab_f, double* u_f, const Geom& gc,
                        const double* e_c, cudaStream_t st);
+void launch_initial_field(const Geom& g, const uint8_t* labels, double* u, uint64_t state, const uint64_t* cols, int K,
+                          int64_t len, cudaStream_t st);
 void launch_abs_max(const double* u, int64_t n, unsigned long long* maxbits, cudaStream_t st);
 void launch_scale(double* u, int64_t n, double s, cudaStream_t st);
 void launch_gather(const int64_t* idx, int64_t n_int, const double* f, const int32_t* ghost_slot,

@@ -1109,6 +1109,47 @@ bool launch_band_coop(const BandArgs& a, double* x, const int64_t* goff, int ngr
   return e == cudaSuccess;
 }
 
+// Seeded initial field (reference solver.py:205-213, rng.py:14-56): value i of the xorshift64* stream
+// on flat node i, 0 on inactive nodes.  The stream is cut into lanes of `len` values; thread l jumps
+// to its lane's start state with the GF(2) powers of the state update (cols[b] = the 64 column images
+// of step^(len * 2^b)), then steps through its lane.  Bit for bit the sequential stream.
+__global__ void __launch_bounds__(128) initial_field_kernel(Geom g, const uint8_t* __restrict__ lab, double* __restrict__ u,
+                                                            uint64_t state, const uint64_t* __restrict__ cols, int K,
+                                                            int64_t len, int64_t nflat) {
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t i = l * len;
+  if (i >= nflat) return;
+  uint64_t s = state;
+  for (int b = 0; b < K; ++b)
+    if ((l >> b) & 1) {
+      uint64_t o = 0;
+      const uint64_t* c = cols + 64 * b;
+      for (int k = 0; k < 64; ++k) o ^= ((s >> k) & 1ull) ? __ldg(c + k) : 0ull;
+      s = o;
+    }
+  const int64_t end = min(nflat, i + len);
+  int64_t row = i / g.n, col = i - row * g.n;
+  for (; i < end; ++i) {
+    s ^= s >> 12;
+    s ^= s << 25;
+    s ^= s >> 27;
+    const uint64_t v = s * 2685821657736338717ull;
+    const int64_t pos = row * g.P + col + OFF;
+    u[pos] = lab[pos] == INACTIVE ? 0.0 : 2.0 * ((double)(v >> 11) * 0x1.0p-53) - 1.0;
+    if (++col == g.n) {
+      col = 0;
+      ++row;
+    }
+  }
+}
+
+void launch_initial_field(const Geom& g, const uint8_t* labels, double* u, uint64_t state, const uint64_t* cols, int K,
+                          int64_t len, cudaStream_t st) {
+  const int64_t nflat = g.rows * g.n;
+  const int64_t lanes = (nflat + len - 1) / len;
+  initial_field_kernel<<<(unsigned)((lanes + 127) / 128), 128, 0, st>>>(g, labels, u, state, cols, K, len, nflat);
+}
+
 __global__ void abs_max_kernel(const double* __restrict__ u, int64_t n, unsigned long long* maxbits) {
   double am = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;

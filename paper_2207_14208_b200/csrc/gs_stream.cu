@@ -250,17 +250,13 @@ __global__ void __launch_bounds__(32) gs_stream_kernel(GsArgs a) {
 size_t gs_stream_smem_per_warp() { return sizeof(WarpRing); }
 
 void configure_gs_diag();
-void configure_gs_macro();
 void configure_dense_gemv();
 
-void configure_gs_rows();
 void configure_gs_kernels() {
   const int smem = (int)sizeof(WarpRing);  // one warp per CTA
   cudaFuncSetAttribute(gs_stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(gs_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   configure_gs_diag();
-  configure_gs_macro();
-  configure_gs_rows();
   configure_gs_chain();
   configure_dense_gemv();
 }

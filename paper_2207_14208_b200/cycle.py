@@ -173,6 +173,11 @@ class CycleDriver:
         u[fine.labels == INACTIVE] = 0.0
         return u
 
+    def _device_initial_field(self, seed):
+        """Backends that can draw `initial_field(seed)` where the iterate lives
+        do so and return True."""
+        return False
+
     def run_cycle(self, u=None):
         """One cycle in place.  With ``u`` given (host array) it is uploaded,
         cycled and copied back, like the reference's ``run_cycle(u)``."""
@@ -187,10 +192,13 @@ class CycleDriver:
     def solve(self, u=None, cycles=None, tol=0.0, seed=42):
         cfg = self.cycle_cfg
         cycles = cfg.cycles if cycles is None else cycles
-        if u is None:
-            u = self.initial_field(seed)
         self._set_data(self.f_fine, self.g_fine)
-        self._put_u(np.ascontiguousarray(u, dtype=np.float64))
+        if u is None and self._device_initial_field(seed):
+            u = np.empty(self.plans[0].n_nodes)  # filled by _fetch_u; the field itself never visits the host
+        else:
+            if u is None:
+                u = self.initial_field(seed)
+            self._put_u(np.ascontiguousarray(u, dtype=np.float64))
         ln_scale = 0.0
         ln_norms = []
 

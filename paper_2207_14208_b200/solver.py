@@ -302,6 +302,16 @@ class MultigridSolver(CycleDriver):
             return u
         return super()._fetch_u(u)
 
+    def _device_initial_field(self, seed):
+        # the whole stream on the GPU (GF(2) jump-ahead per 64-value lane): no 1e8..1e9 host draws and no
+        # upload of the iterate for measure_rho at 512^3 / 1024^3
+        from .geometry import ELIMINATED
+
+        fine = self.plans[0]
+        idx = np.flatnonzero(fine.labels == ELIMINATED)
+        self.ctx.initial_field(seed, fine.n_nodes, idx, self.eliminated_values[idx])
+        return True
+
     def _run_cycle(self):
         self.ctx.cycle(1)
 

@@ -239,15 +239,15 @@ def test_batched_solves_match_individual(gpu_available):
     assert rho_got == rho_want
 
 
-@pytest.mark.parametrize("edge,grid", [("0", "0"), ("1", "0"), ("0", "1"), ("0", "3"), ("1", "3")])
-def test_gs_variants_pores64_match_reference(edge, grid, gpu_available, monkeypatch):
-    """The opt-in per-cell row-above hand-off of the 3-D GS kernel
-    (GMG_GS_EDGE=1) and the default batch hand-off give the reference's
-    solve bit for bit (pores 64^3: empty tasks, all levels on gs_macro).
-    GMG_GS_GRID caps the GS grid so that every CTA loops over several task
-    tickets (re-initialising its barriers and reusing its shared-memory rings
-    with stale data from the previous task), as at 512^3 and 1024^3."""
-    monkeypatch.setenv("GMG_GS_EDGE", edge)
+@pytest.mark.parametrize("chain,grid", [("1", "0"), ("1", "1"), ("1", "3"), ("0", "0"), ("0", "3")])
+def test_gs_variants_pores64_match_reference(chain, grid, gpu_available, monkeypatch):
+    """Both 3-D GS kernels (gs_chain.cu, production; GMG_GS_CHAIN=0: the
+    lane-diagonal ring kernel gs_diag.cu) give the reference's solve bit for
+    bit (pores 64^3: empty tasks, trimmed plane ranges).  GMG_GS_GRID caps the
+    GS grid so that every CTA loops over several task tickets
+    (re-initialising its barriers and reusing its shared-memory ring with
+    stale data from the previous task), as at 512^3 and 1024^3."""
+    monkeypatch.setenv("GMG_GS_CHAIN", chain)
     monkeypatch.setenv("GMG_GS_GRID", grid)
     rec = GU.record("pores64")
     plans, solver = _pores64_solver("superlu")
@@ -258,3 +258,23 @@ def test_gs_variants_pores64_match_reference(edge, grid, gpu_available, monkeypa
     u2, rep2 = solver.solve(u=np.zeros(plans[0].n_nodes), cycles=rec["cycles"])
     assert rep2.residual_norms == rep.residual_norms
     assert GU.digest(u2) == rec["solve"]["u_digest"]
+
+
+def test_device_initial_field_matches_host_stream(gpu_available):
+    """The seeded initial iterate drawn on the device (GF(2) jump-ahead
+    per 64-value lane, gmg_initial_field) is the reference's sequential
+    XorShift64Star stream bit for bit (solver.py:205-213, rng.py:14-56),
+    with the prescribed values on eliminated nodes and 0 on inactive ones."""
+    from paper_2207_14208_b200.geometry import ELIMINATED
+
+    plans, s3 = _pores64_solver("superlu")
+    rng = np.random.default_rng(5)
+    elim = plans[0].labels == ELIMINATED
+    assert elim.any()
+    s3.eliminated_values = np.where(elim, rng.standard_normal(plans[0].n_nodes), 0.0)
+    _, s2 = device_solver("disk64")
+    for s, seed in ((s3, 42), (s3, 7), (s2, 42)):
+        want = s.initial_field(seed)
+        assert s._device_initial_field(seed)
+        got = s._get_u()
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), seed

@@ -1,4 +1,4 @@
-"""Compare one GS sweep of the gs_chain kernel with gs_rows (GMG_GS_CHAIN=0) on
+"""Compare one GS sweep of the gs_chain kernel with gs_diag (GMG_GS_CHAIN=0) on
 the same random input; report where they differ.  usage: gs_cmp.py c4:64 [level]"""
 import os
 import sys

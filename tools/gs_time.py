@@ -1,6 +1,6 @@
 """Per-level GS sweep time (CUDA events on the launch stream) for the GS
-kernels selectable at context creation (GMG_GS_ROWS=1: gs_rows.cu, 0:
-gs_macro.cu), with the SURVEY 8(d) algorithmic bytes (24 B per internal node).
+kernels selectable at context creation (variant 2: gs_chain.cu, the production
+kernel; 1: GMG_GS_CHAIN=0, gs_diag.cu), with the SURVEY 8(d) algorithmic bytes (24 B per internal node).
 
 usage: python tools/gs_time.py c4:512 [reps] [variants, e.g. 1,0]
 """
@@ -22,7 +22,7 @@ import _plans
 setup, plans, f, g, e = _plans.load(sys.argv[1])
 PEAK = 6540.2
 for v in variants:
-    os.environ["GMG_GS_CHAIN"] = "1" if v == 2 else "0"  # 2: gs_chain.cu, 1: gs_rows.cu
+    os.environ["GMG_GS_CHAIN"] = "1" if v == 2 else "0"  # 2: gs_chain.cu, 1: gs_diag.cu
     solver = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, device=0,
                                         coarse_backend="device-inverse")
     ctx = solver.ctx

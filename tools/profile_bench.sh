@@ -9,7 +9,7 @@ KERN='regex:^(gs_|ghost_|residual_|restrict_|interp_add|band_|abs_max|scale_kern
 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KERN" -c 3000 --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 if [ "${FULL:-0}" = "1" ]; then
-  ncu --set full --clock-control none --import-source on -k regex:"${GS_KERNEL:-gs_macro_kernel}" -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:"${GS_KERNEL:-gs_chain_kernel}" -c 1 \
       -o gpurun_out/gs_diag_full $CMD > gpurun_out/ncu_full.log 2>&1
   tail -2 gpurun_out/ncu_full.log
 fi

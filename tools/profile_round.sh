@@ -13,7 +13,7 @@ KERN='regex:^(gs_|ghost_|residual_|restrict_|res_restrict|interp_add|band_|abs_m
 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KERN" -c 3000 --csv \
     --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
 if [ "${FULL:-1}" = "1" ]; then
-  ncu --set full --clock-control none --import-source on -k regex:"${GS_KERNEL:-gs_macro_kernel}" -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:"${GS_KERNEL:-gs_chain_kernel}" -c 1 \
       -o gpurun_out/${TAG}_gs_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
   tail -n2 gpurun_out/${TAG}_ncu_full.log
 fi
