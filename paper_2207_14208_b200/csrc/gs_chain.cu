@@ -70,11 +70,18 @@ namespace {
 #define GS_CHAIN_TRACE 0
 #endif
 constexpr int CW = GS_CHAIN_COLS;             // columns per task = lanes per half-warp
-constexpr int CH = 4;                         // chains (rows) per lane
+constexpr int CH = 2;                         // chains (rows) per lane
 constexpr int RR = GS_CHAIN_ROWS;             // rows per task
-static_assert(CW == 16 && RR == 2 * CH, "lane layout: two half-warps of 16 columns, four rows each");
+static_assert(CW == 16 && RR == 4 * CH, "lane layout: two warps of 8 columns, four row groups of two rows each");
+#ifndef GS_CHAIN_SHB
+#define GS_CHAIN_SHB 8
+#endif
+constexpr int SHB = GS_CHAIN_SHB;             // steps warp B runs behind warp A (>= 7 + KB - 1)
 #ifndef GS_CHAIN_CP
 #define GS_CHAIN_CP 4  // 512^3: 1.70 ms at 4, 1.76 at 8, 2.05 at 2 (with KB = 2)
+#endif
+#ifndef GS_CHAIN_ADAPT
+#define GS_CHAIN_ADAPT 0
 #endif
 #ifndef GS_CHAIN_G
 #define GS_CHAIN_G 2
@@ -92,11 +99,11 @@ constexpr int UPL = (RR + 2) * UROWB;         // rows rowbase-1 .. rowbase+8 of 
 constexpr int FPL = RR * CW * 8;              // 1024 B
 constexpr int F_OFF = NS * UPL;
 constexpr int RING = NS * (UPL + FPL);
-constexpr int SKEW = (CW - 1) + (RR - 1);     // steps between the first and the last lane/chain on a plane
-constexpr int NWARPS = 4;                     // compute, TMA loader, writer, cells
+constexpr int SKEW = (CW / 2 - 1) + (RR - 1) + SHB;  // steps between the first and the last lane/chain on a plane
+constexpr int NWARPS = 5;                     // compute A, compute B, TMA loader, writer, cells
 constexpr int BIG = 1 << 30;
 #ifndef GS_CHAIN_KB
-#define GS_CHAIN_KB 4
+#define GS_CHAIN_KB 2  // 512^3: 1.70 ms at (KB, SHB) = (2, 8), 1.73 at (4, 10) and (1, 7)
 #endif
 constexpr int KB = GS_CHAIN_KB;                         // compute steps per readiness check
 #ifndef GS_CHAIN_PFD
@@ -110,9 +117,8 @@ static_assert((G * UPL) % 128 == 0 && (G * FPL) % 128 == 0 && F_OFF % 128 == 0 &
 struct __align__(128) ChCtl {
   unsigned long long bar[NG];
   int task;
-  int rot;         // role rotation of this CTA
   int lready;      // planes < lready (from P0-1 on) have landed
-  int cstep;       // compute steps < cstep are complete
+  int cstep[2];    // steps < cstep[w] of compute warp w are complete
   int wfree;       // ring space of planes < wfree may be refilled
   int bready[CW];  // per column: planes < bready[j] have the row above in the ring
   int cready[RR];  // per row: planes < cready[I] have the left column in the ring
@@ -122,12 +128,26 @@ constexpr size_t CH_SMEM = (size_t)RING + sizeof(ChCtl);
 static_assert(2 * (CH_SMEM + 1024) <= 228 * 1024, "two CTAs per SM");
 #endif
 
+// Cells are self-validating 16-byte words (value, tag), written and read with single 128-bit accesses
+// that bypass L1 (.cg: L2 is the point of coherence); no ordering between cells is needed, so weak
+// accesses do (GS_CHAIN_STRONG=1: relaxed.gpu accesses, for A/B timing).
+#ifndef GS_CHAIN_STRONG
+#define GS_CHAIN_STRONG 0
+#endif
 __device__ __forceinline__ void cell_put(double2* p, double v, double tag) {
+#if GS_CHAIN_STRONG
   asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v), "d"(tag) : "memory");
+#else
+  asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v), "d"(tag) : "memory");
+#endif
 }
 __device__ __forceinline__ double2 cell_get(const double2* p) {
   double2 v;
+#if GS_CHAIN_STRONG
   asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+#else
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+#endif
   return v;
 }
 __device__ __forceinline__ void hint_put(long long* p, long long v) {
@@ -231,16 +251,8 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
   // advances only after every CTA of this launch has read it)
   const int seq = *(volatile int*)a.ctl + 1;
   const long long hseq = (long long)seq << 32;  // cell tags and progress hints of this sweep: hseq | plane
-  // roles of the CTA's four warps (0 compute, 1 TMA loader, 2 writer, 3 cells), rotated by two for
-  // CTAs in odd hardware warp-slot groups so that the compute warps of the two CTAs of an SM sit on
-  // different schedulers
-  if (threadIdx.x == 0) {
-    unsigned wid;
-    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
-    S.rot = a.rot ? (int)((wid >> 2) & 1u) * 2 : 0;
-  }
-  __syncthreads();
-  const int role = (warp + S.rot) & 3;
+  // roles of the CTA's five warps: 0, 1 compute (columns 0-7 / 8-15), 2 TMA loader, 3 writer, 4 cells
+  const int role = warp;
 
   for (;;) {
     if (threadIdx.x == 0) {
@@ -283,23 +295,32 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
     long long* const hint_out = (bout || cout_) ? a.hint + (size_t)cb * 16 : nullptr;
     if (threadIdx.x == 0) {
       S.lready = P0 - 1;
-      S.cstep = 0;
+      S.cstep[0] = 0;
+      S.cstep[1] = 0;
       S.wfree = P0 - 1;
     }
     if (threadIdx.x < CW) S.bready[threadIdx.x] = bin ? P0 : BIG;
     if (threadIdx.x < RR) S.cready[threadIdx.x] = cin ? P0 : BIG;
     __syncthreads();
 
-    if (role == 0) {
+    if (role < 2) {
       // ============================ compute ==============================
-      // Steps run in blocks of KB: the planes / cells a lane needs during a
-      // block are checked once at its start (one warp-uniform loop), and every
-      // lane executes the same straight-line step.  A chain needs no "active"
-      // predicate: outside [P0, P1] and on rows / columns outside the grid's
-      // interior its mask bits are zero, so it only carries the old values
-      // along (m = old, no store), which also primes prev / old for plane P0.
+      // Two warps: warp A (role 0) owns columns k0 .. k0+7 of the task, warp B
+      // (role 1) columns k0+8 .. k0+15 and runs SHB steps behind, taking A's
+      // column 7 from the ring.  Lane (g, j) of a warp owns its column j and
+      // the rows 2g, 2g+1.  Steps run in blocks of KB: the planes / cells /
+      // (for B) steps of A that a lane needs during a block are checked once at
+      // its start (one warp-uniform loop), and every lane executes the same
+      // straight-line step.  A chain needs no "active" predicate: outside
+      // [P0, P1] and on rows / columns outside the grid's interior its mask
+      // bits are zero, so it only carries the old values along (m = old, no
+      // store), which also primes prev / old for plane P0.
+      const int wB = role;
+      const int SH = wB ? SHB : 0;
+      const int Tw = T > 0 ? (P1 - P0) + (CW / 2 - 1) + (RR - 1) + SH + 1 : 0;
       if (T > 0) {
-        const int h = lane >> 4, j = lane & 15;
+        const int g4 = lane >> 3, j = lane & 7;
+        const int col = (CW / 2) * wB + j;
         const unsigned uend = ubase + (unsigned)(NS * UPL);
         const unsigned fend = fbase + (unsigned)(NS * FPL);
         // internal-node bits of each chain's line along the planes: three words A, B, C cover the
@@ -308,43 +329,43 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
         // step later would stall the whole warp on the scoreboard)
         uint32_t mA[CH], mB[CH], mC[CH], mD[CH];
         const uint32_t* mp[CH];
-        int wbw = floordiv(P0 - SKEW, 32);
+        int wbw = floordiv(P0 - SKEW - SH, 32);
         const int wmax = N >> 5;
         const size_t wstride = (size_t)n * g.P;
 #pragma unroll
         for (int i = 0; i < CH; ++i) {
-          const int row = min(rowbase + CH * h + i, N);
-          mp[i] = a.pmask + (size_t)row * g.P + (k0 + j + OFF);
+          const int row = min(rowbase + CH * g4 + i, N);
+          mp[i] = a.pmask + (size_t)row * g.P + (k0 + col + OFF);
           mA[i] = wbw >= 0 ? ldg_u32(mp[i] + (size_t)wbw * wstride) & wclip(wbw, P0, P1) : 0u;
-          mB[i] = wbw + 1 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 1) * wstride) & wclip(wbw + 1, P0, P1) : 0u;
-          mC[i] = wbw + 2 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 2) * wstride) & wclip(wbw + 2, P0, P1) : 0u;
-          mD[i] = wbw + 3 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 3) * wstride) & wclip(wbw + 3, P0, P1) : 0u;
+          mB[i] = wbw + 1 >= 0 && wbw + 1 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 1) * wstride) & wclip(wbw + 1, P0, P1) : 0u;
+          mC[i] = wbw + 2 >= 0 && wbw + 2 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 2) * wstride) & wclip(wbw + 2, P0, P1) : 0u;
+          mD[i] = wbw + 3 >= 0 && wbw + 3 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 3) * wstride) & wclip(wbw + 3, P0, P1) : 0u;
         }
         int fl0;
         do {
           fl0 = ld_flag(&S.lready);
         } while (!__all_sync(0xffffffffu, fl0 > P0));
         const unsigned z0 = dep0(fl0);
-        if (tr && lane == 0) tr[3] = gtimer();
+        if (tr && threadIdx.x == 0) tr[3] = gtimer();
 #if GS_CHAIN_TRACE
         long long c_wait = 0;
         const long long c_start = clock64();
 #endif
         const double h2 = g.h2, inv = g.inv;
-        const bool jfirst = j == 0, h0 = h == 0;
-        const bool wantB = h0 && bin, wantC = jfirst && cin;
-        // flags this lane polls: the row-above cells of its column (half-warp 0), the left-column
-        // cells of its four rows (lane 0 of each half-warp); lanes that need none poll lready again
-        const int* const fB = wantB ? &S.bready[j] : &S.lready;
+        const bool jfirst = j == 0, g0 = g4 == 0;
+        const bool wantB = g0 && bin, wantC = jfirst && cin && !wB;
+        // flags this lane polls: the row-above cells of its column (row group 0), the left-column cells
+        // of its two rows (lane 0 of each row group of warp A); lanes that need none poll lready again
+        const int* const fB = wantB ? &S.bready[col] : &S.lready;
         const int* fC[CH];
 #pragma unroll
-        for (int i = 0; i < CH; ++i) fC[i] = wantC && CH * h + i < Rb ? &S.cready[CH * h + i] : &S.lready;
-        // Ring addresses.  ub[i] / fb[i]: chain i's current plane, at row rowbase + 4h, column k0 + j
-        // (chain i's own node is i rows further: an immediate offset); chain i + 1 is one plane behind
-        // chain i, so the addresses rotate through the chains and only the leading plane's is computed.
-        const int ps = P0 - j - CH * h;  // plane of chain 0 at step 0
-        const unsigned lane_u = (unsigned)(1 + CH * h) * UROWB + (unsigned)(2 + j) * 8u + z0;
-        const unsigned lane_f = (unsigned)(CH * h) * (CW * 8) + (unsigned)j * 8u + z0;
+        for (int i = 0; i < CH; ++i) fC[i] = wantC && CH * g4 + i < Rb ? &S.cready[CH * g4 + i] : &S.lready;
+        // Ring addresses.  ub[i] / fb[i]: chain i's current plane, at row rowbase + 2g, column k0 + col
+        // (chain i's own node is i rows further: an immediate offset); chain 1 is one plane behind
+        // chain 0, so the addresses move down the chains and only the leading plane's is computed.
+        const int ps = P0 - j - CH * g4 - SH;  // plane of chain 0 at step 0
+        const unsigned lane_u = (unsigned)(1 + CH * g4) * UROWB + (unsigned)(2 + col) * 8u + z0;
+        const unsigned lane_f = (unsigned)(CH * g4) * (CW * 8) + (unsigned)col * 8u + z0;
         unsigned ub[CH], fb[CH];
         double prev[CH], oo[CH];
 #pragma unroll
@@ -359,7 +380,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
         unsigned un = ubase + slot_of(ps + 1) * UPL + lane_u;  // plane above chain 0's
         int p = ps;                 // chain i of this lane is at plane p - i
         int pw = ps - 32 * wbw;     // ... at bit pw - i of the mask window
-        for (int t0 = 0; t0 < T; t0 += KB) {
+        for (int t0 = 0; t0 < Tw; t0 += KB) {
           if (t0 > 0 && (t0 & 31) == 0) {  // next 32 planes of the masks (uniform over the warp)
             ++wbw;
             pw -= 32;
@@ -368,10 +389,10 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
               mA[i] = mB[i];
               mB[i] = mC[i];
               mC[i] = mD[i];
-              mD[i] = wbw + 3 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 3) * wstride) & wclip(wbw + 3, P0, P1) : 0u;
+              mD[i] = wbw + 3 >= 0 && wbw + 3 <= wmax ? ldg_u32(mp[i] + (size_t)(wbw + 3) * wstride) & wclip(wbw + 3, P0, P1) : 0u;
             }
           }
-          {  // readiness of the block's planes (chain 0 leads: planes p .. p + KB - 1, chain i lags i)
+          {  // readiness of the block's planes (chain 0 leads: planes p .. p + KB - 1, chain 1 lags one)
 #if GS_CHAIN_TRACE
             const long long c0 = clock64();
 #endif
@@ -381,16 +402,20 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
             for (;;) {
               const int a1 = ld_flag(&S.lready);
               const int b1 = ld_flag(fB);
+              // warp B reads warp A's column 7 (new) SHB - 7 steps after A wrote it and overwrites the old
+              // values A's column 7 reads as right neighbours SHB - 7 steps after A read them: A must have
+              // finished the first step of this block
+              const int s1 = ld_flag(&S.cstep[0]);
               bool ok = a1 > hi + 1 && (!wantB || b1 > hi);
-              fl = a1 | b1;
+              fl = a1 | b1 | s1;
 #pragma unroll
               for (int i = 0; i < CH; ++i) {
                 const int c1 = ld_flag(fC[i]);
                 const int hc = min(p - i + KB - 1, P1);
-                ok = ok && (!wantC || hc < P0 || c1 > hc || fC[i] == &S.lready);
+                ok = ok && (fC[i] == &S.lready || hc < P0 || c1 > hc);
                 fl |= c1;
               }
-              if (__all_sync(0xffffffffu, ok || !need)) break;
+              if (__all_sync(0xffffffffu, (ok || !need) && (!wB || s1 > t0))) break;
             }
 #if GS_CHAIN_TRACE
             c_wait += clock64() - c0;
@@ -413,9 +438,9 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
 #pragma unroll
             for (int i = 0; i < CH; ++i) {
               fv[i] = ldr(fb[i] + (unsigned)i * (CW * 8));
-              rt[i] = ldr(ub[i] + (unsigned)i * UROWB + 8u);  // old right neighbour (the halo column for lane 15)
+              rt[i] = ldr(ub[i] + (unsigned)i * UROWB + 8u);  // old right neighbour (B's column 0 / the halo column)
             }
-            double rb3 = ldr(ub[CH - 1] + (unsigned)CH * UROWB);  // old row below the lane's last row
+            double rbl = ldr(ub[CH - 1] + (unsigned)CH * UROWB);  // old row below the lane's last row
 #pragma unroll
             for (int i = 0; i < CH; ++i) {
 #if GS_CHAIN_XP & 4
@@ -423,15 +448,16 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
 #else
               lf[i] = __shfl_up_sync(0xffffffffu, prev[i], 1);
 #endif
-              ldr_if(lf[i], ub[i] + (unsigned)i * UROWB - 8u, jfirst);  // lane 0: the halo column (cells)
+              // lane 0 of a row group: the column to the left from the ring (halo column: cells; B: A's column 7)
+              ldr_if(lf[i], ub[i] + (unsigned)i * UROWB - 8u, jfirst);
             }
 #if GS_CHAIN_XP & 4
             double ra0 = prev[CH - 1];
 #else
-            double ra0 = __shfl_up_sync(0xffffffffu, prev[CH - 1], 16);
+            double ra0 = __shfl_up_sync(0xffffffffu, prev[CH - 1], 8);  // row group g - 1's last row
 #endif
-            ldr_if(ra0, ub[0] - UROWB, h0);  // half-warp 0: the halo row (cells)
-            // the four chains op by op (independent dependency chains side by side); chain i reads chain
+            ldr_if(ra0, ub[0] - UROWB, g0);  // row group 0: the halo row (cells)
+            // the chains op by op (independent dependency chains side by side); chain i reads chain
             // i-1's value of the previous step, so every prev[] is read before any is replaced
             double sum[CH], hf[CH], m[CH];
             bool in[CH];
@@ -440,7 +466,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
 #pragma unroll
             for (int i = 0; i < CH; ++i) sum[i] = sum[i] + (i == 0 ? ra0 : prev[i - 1]);
 #pragma unroll
-            for (int i = 0; i < CH; ++i) sum[i] = sum[i] + (i == CH - 1 ? rb3 : pa[i + 1]);
+            for (int i = 0; i < CH; ++i) sum[i] = sum[i] + (i == CH - 1 ? rbl : pa[i + 1]);
 #pragma unroll
             for (int i = 0; i < CH; ++i) sum[i] = sum[i] + lf[i];
 #pragma unroll
@@ -461,7 +487,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
               prev[i] = m[i];
               oo[i] = pa[i];
             }
-            st_flag_if(&S.cstep, t0 + k + 1, lane == 0);  // steps <= t0 + k are complete (stores above included)
+            st_flag_if(&S.cstep[wB], t0 + k + 1, lane == 0);  // steps <= t0 + k are complete (stores above included)
             // next plane: the addresses move down the chains
 #pragma unroll
             for (int i = CH - 1; i > 0; --i) {
@@ -476,17 +502,15 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
           }
         }
         __syncwarp();
-        if (lane == 0) {
-          st_flag(&S.cstep, BIG);
-        }
+        if (lane == 0) st_flag(&S.cstep[wB], BIG);
 #if GS_CHAIN_TRACE
-        if (tr && lane == 0) {
+        if (tr && threadIdx.x == 0) {
           tr[4] = clock64() - c_start;
           tr[5] = c_wait;
         }
 #endif
       }
-    } else if (role == 1) {
+    } else if (role == 2) {
       // ============================ TMA loader ===========================
       // Groups of G planes (from the one holding P0-1 to the one holding
       // P1+1) into group slot (group mod NG) once every plane of its previous
@@ -541,7 +565,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
         }
 #endif
       }
-    } else if (role == 2) {
+    } else if (role == 3) {
       // ============================ writer ===============================
       // First the cells of planes without internal nodes (old values, which
       // no one changes), then every finished plane back to HBM.
@@ -563,12 +587,14 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
         const bool isB = lane < CW;
         const int q_ = isB ? lane : lane - CW;  // column j / row I
         const bool pushes = isB ? bout != nullptr : (cout_ != nullptr && q_ < RR && q_ < Rb);
-        const int lagp = isB ? q_ + (RR - 1) : (CW - 1) + q_;
+        // the compute warp that produces the lane's cells, and the step after which they are final
+        const int cw_ = isB ? (q_ >= CW / 2 ? 1 : 0) : 1;
+        const int lagp = isB ? (q_ & (CW / 2 - 1)) + (RR - 1) + (cw_ ? SHB : 0) : (CW / 2 - 1) + q_ + SHB;
         const unsigned srco = isB ? (unsigned)RR * UROWB + (unsigned)(2 + q_) * 8u : (unsigned)(1 + q_) * UROWB + (unsigned)(CW + 1) * 8u;
         const int cstride = isB ? CW : RR;
         const unsigned uend = ubase + (unsigned)(NS * UPL);
-        int cs = 0;
-        while ((cs = ld_flag(&S.cstep)) < 1) {
+        int cs = 0, csw = 0;
+        while ((cs = ld_flag(&S.cstep[0])) < 1) {
         }
         // (plane P0-1 is read by every chain on its way to P0: its slot is freed with plane P0's)
         // cell source / destination of plane qc, write-back source / destination of plane qw
@@ -591,15 +617,19 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
         long long w_wait = 0, w_busy = 0, w_t = clock64();
 #endif
         while (qw <= P1) {
-          cs = ld_flag(&S.cstep);
+          {
+            const int ca = ld_flag(&S.cstep[0]);
+            csw = ld_flag(&S.cstep[1]);  // warp B finishes every plane last
+            cs = cw_ ? csw : ca;
+          }
 #if GS_CHAIN_TRACE
           {
             const long long now = clock64();
-            if (cs >= (qw - P0) + SKEW + 1) w_busy += now - w_t; else w_wait += now - w_t;
+            if (csw >= (qw - P0) + SKEW + 1) w_busy += now - w_t; else w_wait += now - w_t;
             w_t = now;
           }
 #endif
-          const unsigned z = dep0(cs);
+          const unsigned z = dep0(cs | csw);
           if (pushes)
             while (qc <= P1 && cs > (qc - P0) + lagp) {
               cell_put(cdst, ldr(csrc + z), __longlong_as_double(ctag));
@@ -613,7 +643,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
             }
           __syncwarp();
           const int qw0 = qw;
-          while (qw <= P1 && cs >= (qw - P0) + SKEW + 1) {  // plane qw is final once step SKEW is done
+          while (qw <= P1 && csw >= (qw - P0) + SKEW + 1) {  // plane qw is final once warp B's step SKEW is done
             double v[RR / 2];
 #pragma unroll
             for (int w = 0; w < RR / 2; ++w) v[w] = ldr(wsrc + z + (unsigned)(2 * w) * UROWB);
@@ -653,15 +683,22 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
         const unsigned dsto = isB ? (unsigned)(2 + q_) * 8u : (unsigned)(1 + q_) * UROWB + 8u;
         int* const ready = isB ? &S.bready[q_] : &S.cready[q_];
         int p = P0;
+#if GS_CHAIN_ADAPT
+        int want = 1;  // cells per poll: 1 while the upstream has nothing new, doubling up to CP while it is ahead
+#else
+        constexpr int want = CP;
+#endif
         while (p <= P1) {
           // the next CP cells of this lane, whether or not the upstream task has produced them yet (their
-          // tags decide); only planes the ring already holds
+          // tags decide); only planes the ring already holds.  One poll in flight per lane: a second
+          // one half a round trip later was measured slower (1.80 vs 1.70 ms at 512^3; the extra L2
+          // traffic lengthens every round trip), as were CP = 8 and 16.
           const int top = min(P1, ld_flag(&S.lready) - 1);
           double2 v[CP];
 #pragma unroll
           for (int k = 0; k < CP; ++k) {
             const int q = p + k;
-            v[k] = q <= top ? cell_get(src + (size_t)q * stride + q_) : make_double2(0.0, -1.0);
+            v[k] = q <= top && k < want ? cell_get(src + (size_t)q * stride + q_) : make_double2(0.0, -1.0);
           }
           int adv = 0;
 #pragma unroll
@@ -678,6 +715,9 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
             p += adv;
             st_flag(ready, p);
           }
+#if GS_CHAIN_ADAPT
+          want = adv == want ? min(2 * want, CP) : 1;
+#endif
         }
       }
     }
