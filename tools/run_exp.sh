@@ -1,2 +1,3 @@
-timeout 600 python tools/gs_time.py c4:512 5 2 > gpurun_out/r03d_gs_time.txt 2>&1; cat gpurun_out/r03d_gs_time.txt
-for v in ad4 ad8; do echo "== $v"; GMG_LIB_OVERRIDE=build/exp_$v/libghostmg_b200.so timeout 120 python tools/gs_cmp.py c3:128 2>&1 | head -1; GMG_LIB_OVERRIDE=build/exp_$v/libghostmg_b200.so timeout 600 python tools/gs_time.py c4:512 5 2 > gpurun_out/r03d_gs_time_$v.txt 2>&1; cat gpurun_out/r03d_gs_time_$v.txt; done
+TAG=r02 bash tools/profile_round.sh
+for c in c3 c1 c2d; do timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-bitexact > gpurun_out/r02_bench_$c.json 2> gpurun_out/r02_bench_$c.log; tail -1 gpurun_out/r02_bench_$c.log; done
+ls -la gpurun_out/r02_*
