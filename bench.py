@@ -55,7 +55,7 @@ def log(*a):
 
 
 # ---------------------------------------------------------------- workload
-def build_workload(args):
+def build_workload(args, device=None):
     from paper_2207_14208_b200 import configs as CF
     from paper_2207_14208_b200.cycle import CycleDriver
     from paper_2207_14208_b200.transfer import build_hierarchy
@@ -63,8 +63,9 @@ def build_workload(args):
     builder = CF.CONFIGS[args.config]
     setup = builder(args.N) if args.N else builder()
     t0 = time.time()
+    # device: the per-node label work of the setup (classification, restriction checks) on the GPU
     levels = build_hierarchy(setup.grid, setup.phi, setup.faces, max_levels=setup.cycle.max_levels,
-                             coarsest_min=setup.coarsest_min)
+                             coarsest_min=setup.coarsest_min, device=device)
     t1 = time.time()
     plans, f, g, e = CycleDriver.problem_data(levels, setup.spec, setup.smoother, setup.default_variant)
     if setup.f_seed is not None:
@@ -240,7 +241,7 @@ def run_b200(args, rank, world, local_rank):
     from paper_2207_14208_b200 import _lib
     from paper_2207_14208_b200.solver import MultigridSolver
 
-    setup, plans, f, g, e, setup_times = build_workload(args)
+    setup, plans, f, g, e, setup_times = build_workload(args, device=local_rank)
     t0 = time.time()
     sharded = False
     if world > 1 and plans[0].d == 3:

@@ -94,6 +94,25 @@ int gmg_abs_max_planes(gmg_ctx* ctx, int64_t lo, int64_t hi, double* peak);
 int gmg_initial_field(gmg_ctx* ctx, uint64_t state, const uint64_t* jump_cols, int K, int64_t lane_len,
                       int64_t n_elim, const int64_t* elim_idx, const double* elim_val);
 
+/* ---- setup on the device -------------------------
+ * Node labels of one level for the ball family of level sets (reference
+ * classify, geometry.py:374-416: sign of phi, box faces, internal neighbours):
+ * kind 0 = pore space, domain outside n_balls balls (phi = max_k (r_k - |x - c_k|)),
+ * kind 1 = signed sphere (phi = |x - c| - R).  `axis` holds the N + 1 node
+ * coordinates of one axis, `face_mask` bit 2*axis + side the eliminated faces,
+ * `labels_out` the flat C-order (N+1)^d labels (0 internal, 1 ghost, 2
+ * inactive, 3 eliminated), bit for bit the host classification before the
+ * promotion closure (which, like the ghost geometry, runs on the host). */
+int gmg_setup_classify_balls(int device, int d, int64_t N, const double* axis, int kind, int n_balls,
+                             const double* centers, const double* radii, int face_mask, uint8_t* labels_out);
+/* What the reference's restriction constructors raise (transfer.py:64-114),
+ * checked for every coarse node: flags 1 interior block leaves the box, 2 mixed
+ * block without an internal node, 4 coarse ghost without an in-box ghost /
+ * inactive fine node, 8 / 16 block centre with the wrong fine label. */
+int gmg_setup_check_transfer(int device, int d, int64_t Nf, const uint8_t* lab_f, int64_t Nc, const uint8_t* lab_c,
+                             int* flags_out);
+const char* gmg_setup_last_error(void);
+
 /* Library version (major*10000 + minor*100 + patch). */
 int gmg_version(void);
 

@@ -70,6 +70,9 @@ SIGNATURES = {
     "gmg_profile": (_i, [_p, _i]),
     "gmg_profile_read": (_i, [_p, _i, _i, _p, _p]),
     "gmg_uniform_symmetric": (_i, [ctypes.c_uint64, _i64, _p]),
+    "gmg_setup_classify_balls": (_i, [_i, _i, _i64, _p, _i, _i, _p, _p, _i, _p]),
+    "gmg_setup_check_transfer": (_i, [_i, _i, _i64, _p, _i64, _p, _p]),
+    "gmg_setup_last_error": (ctypes.c_char_p, []),
 }
 
 _lib = None
@@ -351,3 +354,29 @@ def uniform_symmetric_native(seed, n):
     if n:
         load().gmg_uniform_symmetric(int(seed) & ((1 << 64) - 1), int(n), ptr(out))
     return out
+
+
+def setup_classify_balls(device, d, N, axis, kind, centers, radii, face_mask):
+    """Labels of one level on the device (gmg_setup_classify_balls)."""
+    lib = load()
+    axis = np.ascontiguousarray(axis, dtype=np.float64)
+    centers = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, d)
+    radii = np.ascontiguousarray(radii, dtype=np.float64).reshape(-1)
+    out = np.empty((N + 1) ** d, dtype=np.uint8)
+    rc = lib.gmg_setup_classify_balls(device, d, N, ptr(axis), kind, len(radii), ptr(centers), ptr(radii), face_mask,
+                                      ptr(out))
+    if rc != 0:
+        raise GmgError(lib.gmg_setup_last_error().decode())
+    return out
+
+
+def setup_check_transfer(device, d, Nf, lab_f, Nc, lab_c):
+    """Bit mask of failed restriction-block checks (gmg_setup_check_transfer)."""
+    lib = load()
+    lab_f = np.ascontiguousarray(lab_f, dtype=np.uint8)
+    lab_c = np.ascontiguousarray(lab_c, dtype=np.uint8)
+    flags = np.zeros(1, dtype=np.int32)
+    rc = lib.gmg_setup_check_transfer(device, d, Nf, ptr(lab_f), Nc, ptr(lab_c), ptr(flags))
+    if rc != 0:
+        raise GmgError(lib.gmg_setup_last_error().decode())
+    return int(flags[0])

@@ -243,7 +243,12 @@ int dalloc(gmg_ctx* ctx, T** p, int64_t count) {
 template <class T>
 int upload(gmg_ctx* ctx, T** p, const T* host, int64_t count) {
   if (dalloc(ctx, p, count)) return -1;
-  if (count > 0) GMG_CHECK(ctx, cudaMemcpy(*p, host, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice));
+  if (count > 0) {
+    GMG_CHECK(ctx, cudaMemcpy(*p, host, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice));
+    // a copy from pageable memory returns once the data is staged: the DMA itself may still be in flight,
+    // and kernels on the context's non-blocking stream do not wait for the legacy stream
+    GMG_CHECK(ctx, cudaStreamSynchronize(0));
+  }
   return 0;
 }
 
@@ -1503,6 +1508,7 @@ int gmg_set_slab(gmg_ctx* ctx, int li, int64_t lo, int64_t hi) {
       if (q.x > q.y) q = make_int2(1 << 30, -1);
     }
     GMG_CHECK(ctx, cudaMemcpy(l.rw_prange, pr.data(), sizeof(int2) * pr.size(), cudaMemcpyHostToDevice));
+    GMG_CHECK(ctx, cudaStreamSynchronize(0));
   }
   // the slab's ghosts: a contiguous range in lexicographic order, one contiguous range per sweep batch
   auto lb = [&](const std::vector<int32_t>& v, int64_t a, int64_t b, int64_t plane) {
@@ -1607,6 +1613,7 @@ int gmg_set_coarse_inverse(gmg_ctx* ctx, int64_t n, const double* inv, int on_de
   if (dalloc(ctx, &l.cinv, n * n) || dalloc(ctx, &l.cpart, (int64_t)gemv_chunks(n) * n)) return -1;
   GMG_CHECK(ctx, cudaMemcpy(l.cinv, inv, sizeof(double) * (size_t)(n * n),
                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+  GMG_CHECK(ctx, cudaStreamSynchronize(0));  // (copies on the legacy stream; the cycle runs on the context's)
   l.cinv_n = n;
   return 0;
 }
@@ -1652,6 +1659,7 @@ int gmg_set_coarse_nd(gmg_ctx* ctx, int64_t n, int64_t na, int64_t nb, int64_t n
   GMG_CHECK(ctx, cudaMemcpy(l.nd_g, g, sizeof(double) * (size_t)(ns * nab), kind));
   GMG_CHECK(ctx, cudaMemcpy(l.nd_w, w, sizeof(double) * (size_t)(nab * ns), kind));
   GMG_CHECK(ctx, cudaMemcpy(l.nd_si, si, sizeof(double) * (size_t)(ns * ns), kind));
+  GMG_CHECK(ctx, cudaStreamSynchronize(0));
   l.nd_n = n;
   l.nd_a = na;
   l.nd_b = nb;
@@ -1714,6 +1722,7 @@ int gmg_coarse_prog_dense(gmg_ctx* ctx, int64_t m, int64_t k, const double* M, i
   if (dalloc(ctx, &op.M, m * k)) return -1;
   GMG_CHECK(ctx, cudaMemcpy(op.M, M, sizeof(double) * (size_t)(m * k),
                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+  GMG_CHECK(ctx, cudaStreamSynchronize(0));
   const int64_t part = gemv_rect_part_size(m, k);
   if (part > l.cprog_part_n) {
     if (l.cprog_part) cudaFree(l.cprog_part);

@@ -80,6 +80,19 @@ constexpr int SHB = GS_CHAIN_SHB;             // steps warp B runs behind warp A
 #ifndef GS_CHAIN_CP
 #define GS_CHAIN_CP 4  // 512^3: 1.70 ms at 4, 1.76 at 8, 2.05 at 2 (with KB = 2)
 #endif
+// Back-off (ns) of the warps that spin on shared-memory flags -- compute warps waiting for planes /
+// cells, the loader waiting for ring space, the writer waiting for steps.  Four of a CTA's five warps
+// spin most of the time and share the SM's four schedulers with the cells warps, whose poll loop is on
+// the critical path of every hand-off.
+#ifndef GS_CHAIN_NAP_C
+#define GS_CHAIN_NAP_C 0
+#endif
+#ifndef GS_CHAIN_NAP_L
+#define GS_CHAIN_NAP_L 0
+#endif
+#ifndef GS_CHAIN_NAP_W
+#define GS_CHAIN_NAP_W 0
+#endif
 #ifndef GS_CHAIN_ADAPT
 #define GS_CHAIN_ADAPT 0
 #endif
@@ -416,6 +429,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
                 fl |= c1;
               }
               if (__all_sync(0xffffffffu, (ok || !need) && (!wB || s1 > t0))) break;
+              if (GS_CHAIN_NAP_C) __nanosleep(GS_CHAIN_NAP_C);
             }
 #if GS_CHAIN_TRACE
             c_wait += clock64() - c0;
@@ -556,7 +570,10 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
           }
           const int ga0 = ga;
           while (ga < gq && mbar_test(sa(&S.bar[umod(ga, NG)]), (unsigned)(((ga - glo) / NG) & 1))) ++ga;
-          if (ga != ga0) st_flag(&S.lready, ga * G);
+          if (ga != ga0)
+            st_flag(&S.lready, ga * G);
+          else if (GS_CHAIN_NAP_L)
+            __nanosleep(GS_CHAIN_NAP_L);
         }
 #if GS_CHAIN_TRACE
         if (tr) {
@@ -659,6 +676,8 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
           if (qw != qw0) {
             __syncwarp();  // every lane's ring reads of the planes < qw are done
             st_flag_if(&S.wfree, qw, lane == 0);
+          } else if (GS_CHAIN_NAP_W) {
+            __nanosleep(GS_CHAIN_NAP_W);
           }
         }
 #if GS_CHAIN_TRACE
@@ -683,6 +702,9 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
         const unsigned dsto = isB ? (unsigned)(2 + q_) * 8u : (unsigned)(1 + q_) * UROWB + 8u;
         int* const ready = isB ? &S.bready[q_] : &S.cready[q_];
         int p = P0;
+#if GS_CHAIN_TRACE
+        long long rtt_sum = 0, rtt_n = 0, it_n = 0, it_hit = 0;
+#endif
 #if GS_CHAIN_ADAPT
         int want = 1;  // cells per poll: 1 while the upstream has nothing new, doubling up to CP while it is ahead
 #else
@@ -695,11 +717,23 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
           // traffic lengthens every round trip), as were CP = 8 and 16.
           const int top = min(P1, ld_flag(&S.lready) - 1);
           double2 v[CP];
+#if GS_CHAIN_TRACE
+          const long long tq0 = clock64();
+#endif
 #pragma unroll
           for (int k = 0; k < CP; ++k) {
             const int q = p + k;
             v[k] = q <= top && k < want ? cell_get(src + (size_t)q * stride + q_) : make_double2(0.0, -1.0);
           }
+#if GS_CHAIN_TRACE
+          if (p <= top) {  // cycles until the poll's last cell is back (the compare below needs it)
+            long long tq1;  // read the clock only once both the first and the last cell have arrived
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(tq1) : "l"(__double_as_longlong(v[CP - 1].y)), "l"(__double_as_longlong(v[0].y)) : "memory");
+            rtt_sum += tq1 - tq0;
+            ++rtt_n;
+          }
+          ++it_n;
+#endif
           int adv = 0;
 #pragma unroll
           for (int k = 0; k < CP; ++k) {
@@ -714,11 +748,22 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
           if (adv) {
             p += adv;
             st_flag(ready, p);
+#if GS_CHAIN_TRACE
+            ++it_hit;
+#endif
           }
 #if GS_CHAIN_ADAPT
           want = adv == want ? min(2 * want, CP) : 1;
 #endif
         }
+#if GS_CHAIN_TRACE
+        if (tr && lane == 0) {
+          tr[10] = rtt_sum;
+          tr[11] = rtt_n;
+          tr[12] = it_n;
+          tr[13] = it_hit;
+        }
+#endif
       }
     }
     __syncthreads();

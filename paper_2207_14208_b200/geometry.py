@@ -401,9 +401,30 @@ def _sign_negative(grid, phi):
     return (vals < 0.0).reshape(grid.shape), vals
 
 
-def classify(grid, phi, eliminated_faces=()):
+def _device_labels(grid, phi, eliminated_faces, device):
+    """Labels before the promotion closure, computed on GPU `device` for
+    level sets of the ball family (``phi.device_spec()``); None otherwise."""
+    spec = getattr(phi, "device_spec", None)
+    if device is None or spec is None or grid.d not in (2, 3):
+        return None
+    from . import _lib
+
+    kind, centers, radii = spec()
+    mask = 0
+    for axis, side in eliminated_faces:
+        mask |= 1 << (2 * axis + (0 if side == FACE_LOW else 1))
+    return _lib.setup_classify_balls(device, grid.d, grid.N, grid.axis_coords, kind, centers, radii, mask)
+
+
+def classify(grid, phi, eliminated_faces=(), device=None):
     """Label every node and attach ghost geometry (reference
-    geometry.py:374-446)."""
+    geometry.py:374-446).  With ``device`` (a CUDA ordinal) and a level set of
+    the ball family the per-node part -- sign of phi, faces, internal
+    neighbours -- runs on the GPU (bit-identical labels); the ghost geometry
+    and the promotion closure stay here, on the whole ghost batch."""
+    labels = _device_labels(grid, phi, eliminated_faces, device)
+    if labels is not None:
+        return _close_ghosts(Classification(grid, phi, labels, None), phi)
     neg, phi_vals = _sign_negative(grid, phi)
     d, N = grid.d, grid.N
     shape = grid.shape
@@ -441,7 +462,11 @@ def classify(grid, phi, eliminated_faces=()):
     del internal, eliminated, ghost
     labels = labels.reshape(-1)
 
-    cls = Classification(grid, phi, labels, phi_vals)
+    return _close_ghosts(Classification(grid, phi, labels, phi_vals), phi)
+
+
+def _close_ghosts(cls, phi):
+    """Ghost geometry + the promotion closure (geometry.py:419-446)."""
     promoted = np.zeros(0, dtype=np.int64)
     projection_cache = {}
     for _ in range(MAX_CLOSURE_ROUNDS):

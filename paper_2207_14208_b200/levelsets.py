@@ -179,6 +179,11 @@ class SignedSphere(LevelSet):
         with np.errstate(divide="ignore", invalid="ignore"):
             return diff / r[..., None]
 
+    def device_spec(self):
+        """(kind, centers, radii) for gmg_setup_classify_balls (kind 1:
+        the domain is the inside of one ball)."""
+        return 1, self.center.reshape(1, -1), np.array([self.radius])
+
 
 class PoreSpace(LevelSet):
     """Exterior of a union of balls: phi = max_k (r_k - |x - c_k|).
@@ -277,6 +282,11 @@ class PoreSpace(LevelSet):
         dist = np.sqrt(_rowsum([diff[..., a] * diff[..., a] for a in range(self.d)]))
         with np.errstate(divide="ignore", invalid="ignore"):
             return -diff / dist[..., None]
+
+    def device_spec(self):
+        """(kind, centers, radii) for gmg_setup_classify_balls (kind 0:
+        the domain is the outside of every ball)."""
+        return 0, self.centers, self.radii
 
     # -- classify fast path -------------------------------------------------
     def nonnegative_mask(self, grid):

@@ -429,6 +429,6 @@ def build_solver(grid, phi, spec, eliminated_faces=(), smoother=None, cycle=None
     """Hierarchy + B200 solver in one call (reference solver.py:272-279)."""
     cycle = cycle or CycleConfig()
     levels = build_hierarchy(grid, phi, eliminated_faces, max_levels=cycle.max_levels,
-                             coarsest_min=coarsest_min)
+                             coarsest_min=coarsest_min, device=device)
     return MultigridSolver(levels, spec, smoother, cycle, default_variant, device=device,
                            coarse_backend=coarse_backend)

@@ -144,7 +144,7 @@ class Level:
     extrap: ExtrapolationPlan
 
 
-def check_transfer(fine_cls, coarse_cls, chunk=1 << 20, full_below=1 << 22):
+def check_transfer(fine_cls, coarse_cls, chunk=1 << 20, full_below=1 << 22, device=None):
     """Raise what the reference's restriction constructors raise
     (transfer.py:64-114): a coarse internal node whose fine 3^d block leaves
     the box, or whose mixed block holds no internal node; a coarse ghost
@@ -158,6 +158,21 @@ def check_transfer(fine_cls, coarse_cls, chunk=1 << 20, full_below=1 << 22):
     ``full_below`` coarse nodes; above that only the block centres are
     verified."""
     fg, cg = fine_cls.grid, coarse_cls.grid
+    if device is not None and fg.d in (2, 3):
+        # every coarse node on the GPU (gmg_setup_check_transfer): the exhaustive block checks and the
+        # centre checks at any size
+        from . import _lib
+
+        flags = _lib.setup_check_transfer(device, fg.d, fg.N, fine_cls.labels, cg.N, coarse_cls.labels)
+        if flags & 1:
+            raise ResolutionError("interior restriction block leaves the box")
+        if flags & 2:
+            raise EmptyStencil("no internal node under a coarse internal node")
+        if flags & 4:
+            raise EmptyStencil("no ghost/inactive node under a coarse ghost")
+        if flags & 24:
+            raise EmptyStencil("restriction block centre has the wrong label")
+        return
     if cg.n_nodes >= full_below:
         for targets, ok in ((coarse_cls.internal_idx, (INTERNAL,)), (coarse_cls.ghost_idx, (GHOST, INACTIVE))):
             centers = fg.flat_index(2 * cg.multi_index(targets))
@@ -187,11 +202,12 @@ def check_transfer(fine_cls, coarse_cls, chunk=1 << 20, full_below=1 << 22):
                     raise EmptyStencil("no ghost/inactive node under a coarse ghost")
 
 
-def build_hierarchy(grid, phi, eliminated_faces=(), max_levels=None, coarsest_min=4):
+def build_hierarchy(grid, phi, eliminated_faces=(), max_levels=None, coarsest_min=4, device=None):
     """Classify fine to coarse, halving N, with the reference's stop rules:
     odd N, N/2 < coarsest_min, max_levels, or a coarse level that fails to
-    classify or holds a ghost with theta_raw > THETA_TRUST."""
-    fine = classify(grid, phi, eliminated_faces)
+    classify or holds a ghost with theta_raw > THETA_TRUST.  ``device``: CUDA
+    ordinal for the per-node label work (classify, check_transfer)."""
+    fine = classify(grid, phi, eliminated_faces, device=device)
     if fine.n_ghosts and fine.ghost_theta_raw.max() > THETA_TRUST:
         raise ResolutionError(
             "finest grid leaves a ghost farther than the relaxation formula trusts; refine the grid")
@@ -203,7 +219,7 @@ def build_hierarchy(grid, phi, eliminated_faces=(), max_levels=None, coarsest_mi
         if N % 2 or N // 2 < coarsest_min:
             break
         try:
-            coarse = classify(UniformGrid(grid.d, N // 2), phi, eliminated_faces)
+            coarse = classify(UniformGrid(grid.d, N // 2), phi, eliminated_faces, device=device)
         except (ResolutionError, ProjectionError):
             break
         if coarse.n_ghosts and coarse.ghost_theta_raw.max() > THETA_TRUST:
@@ -214,7 +230,7 @@ def build_hierarchy(grid, phi, eliminated_faces=(), max_levels=None, coarsest_mi
         raise ResolutionError("cannot build a second level; grid too coarse")
     levels = [Level(cls=c, extrap=ExtrapolationPlan(c)) for c in chain]
     for a, b in zip(chain[:-1], chain[1:]):
-        check_transfer(a, b)
+        check_transfer(a, b, device=device)
     return levels
 
 

@@ -39,8 +39,10 @@ def c4():
     with open(FIXTURE) as fh:
         rec = json.load(fh)
     setup = CF.config_pores(N=512, cycles=rec["cycles"])
+    # the per-node part of the setup on the GPU (gmg_setup_classify_balls / gmg_setup_check_transfer): the
+    # plan digests below pin it bit for bit at 512^3
     levels = build_hierarchy(setup.grid, setup.phi, setup.faces, max_levels=setup.cycle.max_levels,
-                             coarsest_min=setup.coarsest_min)
+                             coarsest_min=setup.coarsest_min, device=0)
     plans, f, g, e = CycleDriver.problem_data(levels, setup.spec, setup.smoother, setup.default_variant)
     del levels
     f = CF.pore_rhs(setup, plans[0].labels)

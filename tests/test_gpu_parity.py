@@ -278,3 +278,51 @@ def test_device_initial_field_matches_host_stream(gpu_available):
         assert s._device_initial_field(seed)
         got = s._get_u()
         assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), seed
+
+
+@pytest.mark.parametrize("case", ["pores64", "pores128", "ball64", "disk256"])
+def test_device_classification_matches_host(case, gpu_available):
+    """Labels computed on the GPU (gmg_setup_classify_balls) and the whole
+    hierarchy built with the device label work are bit for bit the host's
+    (reference classify, geometry.py:374-446; restriction checks,
+    transfer.py:64-114)."""
+    from paper_2207_14208_b200 import configs as CF
+    from paper_2207_14208_b200.geometry import classify
+    from paper_2207_14208_b200.transfer import build_hierarchy
+
+    setup = {"pores64": lambda: CF.config_pores(N=64), "pores128": lambda: CF.config_pores(N=128),
+             "ball64": lambda: CF.config_ball(64), "disk256": lambda: CF.config_disk(256)}[case]()
+    host = classify(setup.grid, setup.phi, setup.faces)
+    dev = classify(setup.grid, setup.phi, setup.faces, device=0)
+    assert np.array_equal(host.labels, dev.labels)
+    assert np.array_equal(host.ghost_idx, dev.ghost_idx)
+    lv_h = build_hierarchy(setup.grid, setup.phi, setup.faces, max_levels=setup.cycle.max_levels,
+                           coarsest_min=setup.coarsest_min)
+    lv_d = build_hierarchy(setup.grid, setup.phi, setup.faces, max_levels=setup.cycle.max_levels,
+                           coarsest_min=setup.coarsest_min, device=0)
+    assert len(lv_h) == len(lv_d)
+    for a, b in zip(lv_h, lv_d):
+        assert np.array_equal(a.cls.labels, b.cls.labels)
+        assert np.array_equal(a.cls.ghost_theta_raw, b.cls.ghost_theta_raw)
+        assert np.array_equal(a.extrap.band_idx, b.extrap.band_idx)
+
+
+def test_device_check_transfer_flags(gpu_available):
+    """The device restriction checks raise what the host's do on broken label
+    sets (a coarse internal node over a block without internal nodes, a
+    coarse ghost over a block without ghost / inactive nodes)."""
+    from paper_2207_14208_b200 import _lib as L
+    from paper_2207_14208_b200 import configs as CF
+    from paper_2207_14208_b200.geometry import GHOST, INACTIVE, INTERNAL, classify
+    from paper_2207_14208_b200.geometry import UniformGrid
+
+    setup = CF.config_ball(32)
+    fine = classify(setup.grid, setup.phi, setup.faces)
+    coarse = classify(UniformGrid(3, 16), setup.phi, setup.faces)
+    assert L.setup_check_transfer(0, 3, 32, fine.labels, 16, coarse.labels) == 0
+    bad = fine.labels.copy()
+    bad[bad == INTERNAL] = INACTIVE
+    assert L.setup_check_transfer(0, 3, 32, bad, 16, coarse.labels) & (2 | 8)
+    bad = fine.labels.copy()
+    bad[(bad == GHOST) | (bad == INACTIVE)] = INTERNAL
+    assert L.setup_check_transfer(0, 3, 32, bad, 16, coarse.labels) & (4 | 16)

@@ -44,6 +44,11 @@ if nz.any():
           f"waiting for slots {np.median(raw[nz, 5]):.0f}, for cells {np.median(raw[nz, 6]):.0f}")
     print(f"per step (median task): writer waiting for compute {np.median(raw[nz, 6]) / steps:.0f}, writer other {np.median(raw[nz, 7]) / steps:.0f}; "
           f"loader blocked by the ring {np.median(raw[nz, 8]) / steps:.0f}, loader otherwise {np.median(raw[nz, 9]) / steps:.0f}")
+    pol = raw[:, 11] > 0
+    if pol.any():
+        print(f"cells warp (lane 0, per task median): poll round trip {np.median(raw[pol, 10] / raw[pol, 11]):.0f} cycles, "
+              f"{np.median(raw[pol, 12]):.0f} polls of which {np.median(raw[pol, 13]):.0f} accepted something, "
+              f"{np.median(raw[pol, 11]):.0f} with the ring ready")
     i0 = tasks.index((0, 0))
     print(f"task (0,0): cycles {raw[i0, 4]} = {raw[i0, 4] / steps:.0f}/step, slots {raw[i0, 5]}, cells {raw[i0, 6]}")
 print("start/done (us) of tasks (c, b):")

@@ -1,3 +1,1 @@
-TAG=r02 bash tools/profile_round.sh
-for c in c3 c1 c2d; do timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-bitexact > gpurun_out/r02_bench_$c.json 2> gpurun_out/r02_bench_$c.log; tail -1 gpurun_out/r02_bench_$c.log; done
-ls -la gpurun_out/r02_*
+timeout 1700 python -m pytest tests -m gpu -x -q > gpurun_out/r03k_gputest.log 2>&1; tail -5 gpurun_out/r03k_gputest.log
