@@ -179,8 +179,9 @@ struct gmg_ctx {
   bool gs_trace = false;       // record the GS task timeline (GMG_GS_TRACE=1)
   int gs_grid_cap = 0;         // > 0: at most this many GS CTAs (tests the multi-task loop)
   int gs_chain = 1;            // 3-D levels N >= 64: gs_chain.cu (register chains; production); GMG_GS_CHAIN=0:
-                               // the lane-diagonal ring kernel gs_diag.cu (bitwise the same results)
-  int gs_chain_rot = 1;        // its warp-role rotation (GMG_GS_CHAIN_ROT=0: off; timing only)
+                               // the streaming kernel gs_stream.cu (bitwise the same results)
+  int gs_chain_rot = 1;        // (unused: the warp roles are fixed)
+  int gs_diag = 1;             // 2-D levels N >= 64: gs_diag.cu (GMG_GS_DIAG=0: the streaming kernel, bitwise same)
   int64_t band_coop_max = 200000;  // band extensions up to this many nodes: one cooperative launch (GMG_BAND_COOP;
                                    // 128^3 49 -> 40 us, 64^3 47 -> 30 us; 256^3 (533 k nodes) was slower)
   int halo_multi = -1;         // GS halo loader: -1 by level size, 0 two-batch, 1 multi-batch (GMG_GS_HALO)
@@ -1030,7 +1031,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_TRACE")) ctx->gs_trace = e[0] == '1';
   if (const char* e = getenv("GMG_GS_GRID")) ctx->gs_grid_cap = atoi(e);  // cap on GS CTAs (multi-task loop test)
   if (const char* e = getenv("GMG_GS_CHAIN")) ctx->gs_chain = atoi(e);     // 0: gs_diag.cu (bitwise same)
-  if (const char* e = getenv("GMG_GS_CHAIN_ROT")) ctx->gs_chain_rot = atoi(e);
+  if (const char* e = getenv("GMG_GS_DIAG")) ctx->gs_diag = atoi(e);
 #ifdef GMG_EXPERIMENTS
   if (const char* e = getenv("GMG_SIMPLE_GS")) ctx->force_simple_gs = e[0] == '1';
   if (const char* e = getenv("GMG_NO_WS")) ctx->no_ws = e[0] == '1';
@@ -1305,7 +1306,11 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   l.C = (int)((N - 1 + 31) / 32);
   l.stream_gs = N >= 32 && !ctx->force_simple_gs;
   l.ws_gs = N >= 64 && !ctx->force_simple_gs && !ctx->no_ws && encode_fn() != nullptr;
-  l.diag_gs = l.ws_gs;
+  // the lane-diagonal ring kernel (gs_diag.cu) is the 2-D kernel only: in 3-D its results vary from
+  // run to run at 512^3 (tools/gs_cmp.py CMP_MODE=00), so 3-D levels use gs_chain.cu or, with
+  // GMG_GS_CHAIN=0, the streaming kernel
+  l.diag_gs = l.ws_gs && d == 2 && ctx->gs_diag;
+  const bool chain_ok = l.ws_gs && d == 3;
   if (d == 3) {
     l.B1 = l.diag_gs ? 14 : (l.stream_gs ? 16 : 8);
     l.Bn = (int)((N - 1 + l.B1 - 1) / l.B1);
@@ -1326,8 +1331,8 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
         if (row[k] == INTERNAL) im[(size_t)(ln * l.Cm + (k - 1) / 32)] |= 1u << ((k - 1) % 32);
     }
     if (upload(ctx, &l.imask, im.data(), lines * l.Cm)) return -1;
-    if (l.diag_gs) empty_im = im;
-    if (l.ws_gs) {
+    if (l.diag_gs || chain_ok) empty_im = im;
+    if (l.diag_gs) {
       const uint64_t P = (uint64_t)l.g.P;
       if (!make_map(&l.maps.u, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, l.u, P, (uint64_t)l.g.rows, P * 8, 36, 8) ||
           !make_map(&l.maps.f, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, l.f, P, (uint64_t)l.g.rows, P * 8, 32, 8) ||
@@ -1407,7 +1412,7 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   l.ticket = l.progress + 32 * l.C * l.Bn;
 
   l.chain_gs = false;
-  if (d == 3 && N >= 64 && ctx->gs_chain && l.diag_gs && !empty_im.empty()) {
+  if (d == 3 && N >= 64 && ctx->gs_chain && chain_ok && !empty_im.empty()) {
     // gs_chain.cu tasks: 16-column chunk c x block of 8 rows; per task the
     // planes that hold internal nodes; tickets ordered by 4c + 3b (every task
     // after its two upstream tasks; a column hop lags ~4/3 of a row hop)

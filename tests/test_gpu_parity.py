@@ -242,7 +242,7 @@ def test_batched_solves_match_individual(gpu_available):
 @pytest.mark.parametrize("chain,grid", [("1", "0"), ("1", "1"), ("1", "3"), ("0", "0"), ("0", "3")])
 def test_gs_variants_pores64_match_reference(chain, grid, gpu_available, monkeypatch):
     """Both 3-D GS kernels (gs_chain.cu, production; GMG_GS_CHAIN=0: the
-    lane-diagonal ring kernel gs_diag.cu) give the reference's solve bit for
+    streaming kernel gs_stream.cu) give the reference's solve bit for
     bit (pores 64^3: empty tasks, trimmed plane ranges).  GMG_GS_GRID caps the
     GS grid so that every CTA loops over several task tickets
     (re-initialising its barriers and reusing its shared-memory ring with
@@ -326,3 +326,36 @@ def test_device_check_transfer_flags(gpu_available):
     bad = fine.labels.copy()
     bad[(bad == GHOST) | (bad == INACTIVE)] = INTERNAL
     assert L.setup_check_transfer(0, 3, 32, bad, 16, coarse.labels) & (4 | 16)
+
+
+@pytest.mark.parametrize("case", ["pores128", "ball128"])
+def test_gs_chain_matches_stream_kernel(case, gpu_available, monkeypatch):
+    """The production 3-D GS kernel (gs_chain.cu) against the independent
+    streaming kernel (GMG_GS_CHAIN=0) after several sweeps on random data:
+    bitwise equal, also on the sparse ball whose tasks start at even planes
+    (the ring slot of plane P0-1 must outlive the chains' warm-up) -- and
+    equal to itself run to run."""
+    from paper_2207_14208_b200 import configs as CF
+    from paper_2207_14208_b200.cycle import CycleDriver
+    from paper_2207_14208_b200.transfer import build_hierarchy
+
+    setup = CF.config_pores(N=128) if case == "pores128" else CF.config_ball(128)
+    levels = build_hierarchy(setup.grid, setup.phi, setup.faces, max_levels=2, coarsest_min=setup.coarsest_min, device=0)
+    plans, f, g, e = CycleDriver.problem_data(levels, setup.spec, setup.smoother, setup.default_variant)
+    rng = np.random.default_rng(3)
+    u0 = rng.standard_normal(plans[0].n_nodes)
+    f0 = rng.standard_normal(plans[0].n_nodes)
+    out = []
+    for chain in ("1", "1", "0"):
+        monkeypatch.setenv("GMG_GS_CHAIN", chain)
+        ctx = _lib.Context(3, len(plans))
+        for i, p in enumerate(plans):
+            ctx.set_level(i, p)
+        ctx.set_vector(0, _lib.U, u0)
+        ctx.set_vector(0, _lib.F, f0)
+        for _ in range(8):
+            ctx.apply(0, _lib.OP_GS_SWEEP)
+        out.append(ctx.get_vector(0, _lib.U, plans[0].n_nodes).copy())
+        ctx.close()
+    assert np.array_equal(out[0].view(np.uint64), out[1].view(np.uint64))
+    assert np.array_equal(out[0].view(np.uint64), out[2].view(np.uint64))

@@ -16,7 +16,8 @@ rng = np.random.default_rng(1)
 u0 = rng.standard_normal(p.n_nodes)
 f0 = rng.standard_normal(p.n_nodes)
 res = {}
-for v in ("0", "1"):
+MODE = os.environ.get("CMP_MODE", "01")  # which two kernels: 0 gs_diag, 1 gs_chain ("11": chain against itself)
+for slot, v in zip(("0", "1"), MODE):
     os.environ["GMG_GS_CHAIN"] = v
     s = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, device=0, coarse_backend="superlu")
     ctx = s.ctx
@@ -25,7 +26,7 @@ for v in ("0", "1"):
     nsweeps = int(os.environ.get("SWEEPS", 1))
     for _ in range(nsweeps):
         ctx.apply(level, _lib.OP_GS_SWEEP)
-    res[v] = ctx.get_vector(level, _lib.U, p.n_nodes).copy()
+    res[slot] = ctx.get_vector(level, _lib.U, p.n_nodes).copy()
     ctx.close()
 n = p.N + 1
 a = res["0"].reshape(n, n, n)
