@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libghostmg_b200.so")
-SOURCES = ["context.cu", "gs_sweep.cu", "gs_stream.cu", "gs_diag.cu", "gs_chain.cu", "coarse_dense.cu", "setup_ops.cu", "ghost_ops.cu", "grid_ops.cu"]
+SOURCES = ["context.cu", "gs_sweep.cu", "gs_small.cu", "gs_stream.cu", "gs_diag.cu", "gs_chain.cu", "coarse_dense.cu", "setup_ops.cu", "ghost_ops.cu", "grid_ops.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -181,6 +181,8 @@ struct gmg_ctx {
   int gs_chain = 1;            // 3-D levels N >= 64: gs_chain.cu (register chains; production); GMG_GS_CHAIN=0:
                                // the streaming kernel gs_stream.cu (bitwise the same results)
   int gs_chain_rot = 1;        // (unused: the warp roles are fixed)
+  int gs_small = 1;            // levels with N <= 32 (3-D) / N < 64 (2-D): gs_small.cu (GMG_GS_SMALL=0: the multi-CTA
+                               // kernels gs_stream.cu / gs_sweep.cu, bitwise same)
   int gs_diag = 1;             // 2-D levels N >= 64: gs_diag.cu (GMG_GS_DIAG=0: the streaming kernel, bitwise same)
   int64_t band_coop_max = 200000;  // band extensions up to this many nodes: one cooperative launch (GMG_BAND_COOP;
                                    // 128^3 49 -> 40 us, 64^3 47 -> 30 us; 256^3 (533 k nodes) was slower)
@@ -522,6 +524,12 @@ int gs_cap(const gmg_ctx* ctx, int grid) { return ctx->gs_grid_cap > 0 ? std::mi
 // ---- operations ------------------------------------------------------------
 int op_gs(gmg_ctx* ctx, DevLevel& l) {
   Scope s(ctx, 0);
+  if (ctx->gs_small && (l.g.d == 3 ? l.g.N <= 32 : l.g.N < 64)) {
+    // small levels: one CTA, one barrier per hyperplane (gs_small.cu)
+    launch_gs_small(l.g, l.labels, l.u, l.f, ctx->stream);
+    ctx->launches++;
+    return 0;
+  }
   if (l.chain_gs) {
     GsChainArgs r;
     r.g = l.g;
@@ -1032,6 +1040,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_GRID")) ctx->gs_grid_cap = atoi(e);  // cap on GS CTAs (multi-task loop test)
   if (const char* e = getenv("GMG_GS_CHAIN")) ctx->gs_chain = atoi(e);     // 0: gs_diag.cu (bitwise same)
   if (const char* e = getenv("GMG_GS_DIAG")) ctx->gs_diag = atoi(e);
+  if (const char* e = getenv("GMG_GS_SMALL")) ctx->gs_small = atoi(e);
 #ifdef GMG_EXPERIMENTS
   if (const char* e = getenv("GMG_SIMPLE_GS")) ctx->force_simple_gs = e[0] == '1';
   if (const char* e = getenv("GMG_NO_WS")) ctx->no_ws = e[0] == '1';

@@ -86,6 +86,7 @@ size_t gs_chain_smem();
 int gs_chain_group();
 void configure_gs_chain();
 
+void launch_gs_small(const Geom& g, const uint8_t* labels, double* u, const double* f, cudaStream_t st);
 void launch_gs_sweep(const GsArgs& a, int grid, cudaStream_t st);
 void launch_gs_stream(const GsArgs& a, int grid, int warps_per_cta, cudaStream_t st);
 size_t gs_stream_smem_per_warp();

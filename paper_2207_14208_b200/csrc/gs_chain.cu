@@ -584,17 +584,34 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
       }
     } else if (role == 3) {
       // ============================ writer ===============================
-      // First the cells of planes without internal nodes (old values, which
-      // no one changes), then every finished plane back to HBM.
+      // The downstream tasks take a cell for every plane of THEIR range.  For the planes outside this
+      // task's range the values are the old ones, which no one changes: those below P0 are forwarded
+      // first (the consumers need them first), those above P1 after the last plane is written.  Eight
+      // planes per batch so that the loads overlap (the domain of a sparse level set leaves most
+      // planes of most tasks to this loop).
       const double* u = a.u;
       const int h = lane >> 4, j = lane & 15;
-      for (int p = 1; p <= N - 1; ++p) {
-        if (p >= P0 && p <= P1) continue;
-        const int64_t row = (int64_t)p * n + rowbase;
-        if (bout && h == 0) cell_put(bout + (size_t)p * CW + j, __ldcg(u + (row + RR - 1) * g.P + k0 + OFF + j), __longlong_as_double(hseq | (long long)p));
-        if (cout_ && h == 1 && j < Rb)
-          cell_put(cout_ + (size_t)p * RR + j, __ldcg(u + (row + j) * g.P + k0 + OFF + CW - 1), __longlong_as_double(hseq | (long long)p));
-      }
+      // this lane's consumer: (c, b+1) for the row cells (lanes 0..15), (c+1, b) for the column cells
+      const bool fw_on = h == 0 ? bout != nullptr : (cout_ != nullptr && j < Rb);
+      const int2 prd = !fw_on ? make_int2(1, 0) : a.prange[h == 0 ? cb + 1 : cb + a.Bn];
+      const double* const fsrc = h == 0 ? u + ((int64_t)rowbase + RR - 1) * g.P + k0 + OFF + j
+                                        : u + ((int64_t)rowbase + j) * g.P + k0 + OFF + CW - 1;
+      double2* const fdst = h == 0 ? bout + j : cout_ + j;
+      const int fstride = h == 0 ? CW : RR;
+      const int64_t fplane = (int64_t)n * g.P;
+      auto forward = [&](int lo, int hi) {
+        for (int p0 = lo; p0 <= hi; p0 += 8) {
+          double v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = p0 + k <= hi ? __ldcg(fsrc + (int64_t)(p0 + k) * fplane) : 0.0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (p0 + k <= hi)
+              cell_put(fdst + (size_t)(p0 + k) * fstride, v[k], __longlong_as_double(hseq | (long long)(p0 + k)));
+        }
+      };
+      if (fw_on) forward(prd.x, T > 0 ? min(prd.y, P0 - 1) : prd.y);
+      __syncwarp();
       if (T > 0) {
         // Every step: the cells of the values that just became final (row rowbase+7 of column k0+j
         // after step (q - P0) + j + 7, column k0+15 of row rowbase+I after step (q - P0) + 15 + I), read
@@ -686,6 +703,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
           tr[7] = w_busy;
         }
 #endif
+        if (fw_on) forward(max(prd.x, P1 + 1), prd.y);
       }
     } else {
       // ============================ cells ================================

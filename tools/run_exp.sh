@@ -1,5 +1,3 @@
-TAG=r02 bash tools/profile_round.sh
-CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-bitexact"
-ncu --set full --clock-control none -k 'regex:^(residual_march3|restrict_interior|restrict_ghost)' -c 4 -o gpurun_out/r02_cycle_kernels2 -f $CMD > gpurun_out/r02_ncu_cycle2.log 2>&1
-for c in c3 c1 c2d; do timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-bitexact > gpurun_out/r02_bench_$c.json 2> gpurun_out/r02_bench_$c.log; tail -1 gpurun_out/r02_bench_$c.log; done
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r02_bench_reference.json 2> gpurun_out/r02_bench_reference.log; cat gpurun_out/r02_bench_reference.json | cut -c1-400
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -3
+timeout 600 python tools/gs_time.py c3:256 5 2
+for c in c3 c1 c2d; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-bitexact --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['ms_per_step'],3), d['breakdown_ms_per_cycle'])"; done
