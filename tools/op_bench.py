@@ -16,12 +16,11 @@ from paper_2207_14208_b200.cycle import CycleDriver
 from paper_2207_14208_b200.solver import MultigridSolver
 from paper_2207_14208_b200.transfer import build_hierarchy
 
-name, N = sys.argv[1].split(":")
-N = int(N)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _plans
+
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-setup = CF.config_pores(N=N) if name == "c4" else CF.CONFIGS[name](N)
-levels = build_hierarchy(setup.grid, setup.phi, setup.faces, coarsest_min=setup.coarsest_min)
-plans, f, g, e = CycleDriver.problem_data(levels, setup.spec, setup.smoother, setup.default_variant)
+setup, plans, f, g, e = _plans.load(sys.argv[1])
 solver = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle, device=0,
                                     coarse_backend="device-inverse")
 ctx = solver.ctx
