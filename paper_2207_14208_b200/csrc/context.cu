@@ -496,8 +496,16 @@ bool make_map3t(CUtensorMap* m, CUtensorMapDataType t, int esize, void* base, ui
   cuuint64_t strides[2] = {cols * esize, cols * rows * esize};
   cuuint32_t box[3] = {box0, box1, box2};
   cuuint32_t es[3] = {1, 1, 1};
-  return fn(m, t, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  // L2 promotion of the box rows' sector requests (GMG_TMA_L2PROMO=0..3: none, 64, 128, 256 bytes; timing only)
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (const char* e = getenv("GMG_TMA_L2PROMO")) {
+    const int v = atoi(e);
+    promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                   : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                            : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+  return fn(m, t, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool make_map(CUtensorMap* m, CUtensorMapDataType t, void* base, uint64_t cols, uint64_t rows,
