@@ -180,7 +180,7 @@ struct gmg_ctx {
   int gs_grid_cap = 0;         // > 0: at most this many GS CTAs (tests the multi-task loop)
   int gs_chain = 1;            // 3-D levels N >= 64: gs_chain.cu (register chains; production); GMG_GS_CHAIN=0:
                                // the streaming kernel gs_stream.cu (bitwise the same results)
-  int gs_chain_rot = 1;        // (unused: the warp roles are fixed)
+  
   int gs_small = 1;            // levels with N <= 32 (3-D) / N < 64 (2-D): gs_small.cu (GMG_GS_SMALL=0: the multi-CTA
                                // kernels gs_stream.cu / gs_sweep.cu, bitwise same)
   int gs_diag = 1;             // 2-D levels N >= 64: gs_diag.cu (GMG_GS_DIAG=0: the streaming kernel, bitwise same)
@@ -549,7 +549,6 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
     r.C = l.rw_C;
     r.Bn = l.rw_Bn;
     r.cplanes = (int)l.g.n + 32;
-    r.rot = ctx->gs_chain_rot;
     r.ctl = l.rw_ctl;
     r.bcell = l.bcell;
     r.ccell = l.ccell;

@@ -69,7 +69,6 @@ struct GsChainArgs {
   const uint32_t* pmask;  // plane-transposed internal-node bits: word ((p >> 5) * n + r) * P + pos, bit p & 31
   int ntasks, C, Bn;
   int cplanes;            // planes per task in the cell arrays (N + 1 + 32: the chains run past the last plane)
-  int rot;                // rotate the warp roles of CTAs in odd warp-slot groups
   int* ctl;               // [0] sweep sequence, [1] finished CTAs, [2] ticket (zero between sweeps)
   double2* bcell;         // [c * Bn + b][cplanes][GS_CHAIN_COLS]: (value, tag) of the block's last row, per plane
   double2* ccell;         // [c * Bn + b][cplanes][GS_CHAIN_ROWS]: (value, tag) of the chunk's last column

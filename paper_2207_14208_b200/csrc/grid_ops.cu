@@ -1041,10 +1041,18 @@ void launch_band_step(const BandArgs& a, double* x, cudaStream_t st) {
 // BFS groups, the gather, the six Jacobi steps and the scatter as phases of a
 // grid-stride loop separated by grid-wide barriers -- the same per-node
 // arithmetic as band_bfs_kernel / band_*_kernel, without ~11 launches.
-template <int D>
-__global__ void __launch_bounds__(256) band_coop_kernel(BandArgs a, double* __restrict__ x, int64_t g1, int64_t g2,
-                                                        int64_t g3) {
+// SINGLE: one CTA (any block size), __syncthreads() for the phase barriers -- bands of a few thousand
+// nodes, where eleven grid-wide barriers (~2.5 us each) are most of the cooperative launch's time.
+template <int D, bool SINGLE>
+__global__ void __launch_bounds__(SINGLE ? 1024 : 256) band_coop_kernel(BandArgs a, double* __restrict__ x, int64_t g1,
+                                                                        int64_t g2, int64_t g3) {
   cg::grid_group grid = cg::this_grid();
+  auto phase_sync = [&]() {
+    if (SINGLE)
+      __syncthreads();
+    else
+      grid.sync();
+  };
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, ts = (int64_t)gridDim.x * blockDim.x;
   const int64_t s[3] = {a.g.s0, a.g.s1, a.g.s2};
   const int64_t goff[4] = {0, g1, g2, g3};
@@ -1063,14 +1071,14 @@ __global__ void __launch_bounds__(256) band_coop_kernel(BandArgs a, double* __re
         }
       x[i] = seq_sum<2 * D>(t) / (double)__popc(mk);
     }
-    grid.sync();
+    phase_sync();
   }
   for (int64_t q = t0; q < a.nb + a.nfix; q += ts) {
     const double v = q < a.nb ? x[a.idx[q]] : x[a.fixpos[q - a.nb]];
     a.v0[q] = v;
     if (q >= a.nb) a.v1[q] = v;
   }
-  grid.sync();
+  phase_sync();
   for (int it = 0; it < 6; ++it) {
     const double* vin = (it & 1) ? a.v1 : a.v0;
     double* vout = (it & 1) ? a.v0 : a.v1;
@@ -1081,7 +1089,7 @@ __global__ void __launch_bounds__(256) band_coop_kernel(BandArgs a, double* __re
       for (int k = 0; k < D; ++k) t[k] = a.absn[q * D + k] * (vi - vin[a.nbr[q * D + k]]);
       vout[q] = vi - 0.5 * seq_sum<D>(t);
     }
-    grid.sync();
+    phase_sync();
   }
   for (int64_t q = t0; q < a.nb; q += ts) x[a.idx[q]] = a.v0[q];
 }
@@ -1095,17 +1103,24 @@ bool launch_band_coop(const BandArgs& a, double* x, const int64_t* goff, int ngr
   int& o = occ[a.g.d == 3 ? 1 : 0];
   if (o == 0) {
     if (a.g.d == 3)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, band_coop_kernel<3>, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, band_coop_kernel<3, false>, 256, 0);
     else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, band_coop_kernel<2>, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, band_coop_kernel<2, false>, 256, 0);
     if (o < 1) o = 1;
+  }
+  BandArgs aa = a;
+  if (a.nb + a.nfix <= 12288) {  // small band: one CTA, block barriers
+    if (a.g.d == 3)
+      band_coop_kernel<3, true><<<1, 1024, 0, st>>>(aa, x, g[0], g[1], g[2]);
+    else
+      band_coop_kernel<2, true><<<1, 1024, 0, st>>>(aa, x, g[0], g[1], g[2]);
+    return true;
   }
   const int64_t want = (a.nb + a.nfix + 255) / 256;
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, 148 * (int64_t)std::min(o, 2)));
-  BandArgs aa = a;
   void* args[] = {&aa, &x, &g[0], &g[1], &g[2]};
-  cudaError_t e = a.g.d == 3 ? cudaLaunchCooperativeKernel((void*)band_coop_kernel<3>, blocks, 256, args, 0, st)
-                             : cudaLaunchCooperativeKernel((void*)band_coop_kernel<2>, blocks, 256, args, 0, st);
+  cudaError_t e = a.g.d == 3 ? cudaLaunchCooperativeKernel((void*)band_coop_kernel<3, false>, blocks, 256, args, 0, st)
+                             : cudaLaunchCooperativeKernel((void*)band_coop_kernel<2, false>, blocks, 256, args, 0, st);
   return e == cudaSuccess;
 }
 

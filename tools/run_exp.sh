@@ -1,1 +1,6 @@
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline --no-bitexact > gpurun_out/r03n_torchrun1.json 2> gpurun_out/r03n_torchrun1.log; echo rc=$?; cut -c1-300 gpurun_out/r03n_torchrun1.json; tail -3 gpurun_out/r03n_torchrun1.log
+for c in c1 c2d c3 c4; do
+  for gsm in 0 1024 2048 4096 8192; do
+    echo "== $c ghost_small=$gsm"
+    GMG_GHOST_SMALL=$gsm timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --no-bitexact --steps 20 --warmup 5 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['breakdown_ms_per_cycle']['ghost_sweep'])"
+  done
+done
