@@ -208,6 +208,15 @@ int gmg_cycle(gmg_ctx *ctx, int ncycles);
  * Synchronizes. */
 int gmg_residual_norm(gmg_ctx *ctx, int level, double *out);
 
+/* The same, and *peak_lb = max |u| over the level's internal nodes, taken in
+ * the same pass (the values are loaded for the residual anyway): a lower bound
+ * of the max |u| that the renormalisation guard of the solve loop tests
+ * (ref solver.py:239-243, `0 < peak < RENORM_THRESHOLD`), so a caller that
+ * finds it >= the threshold knows the guard's outcome without
+ * gmg_abs_max_scale's pass over the full array.  -1 when it was not computed
+ * (l2 norm, z-slab mode); 0 on a level without internal nodes.  Synchronizes. */
+int gmg_residual_norm_peak(gmg_ctx *ctx, int level, double *out, double *peak_lb);
+
 /* peak = max |u| on level 0; if 0 < peak < threshold, u *= factor and
  * *scaled = 1 (ref solver.py:239-243).  Synchronizes. */
 int gmg_abs_max_scale(gmg_ctx *ctx, double threshold, double factor, double *peak,

@@ -57,6 +57,7 @@ SIGNATURES = {
     "gmg_apply": (_i, [_p, _i, _i, _i]),
     "gmg_cycle": (_i, [_p, _i]),
     "gmg_residual_norm": (_i, [_p, _i, _p]),
+    "gmg_residual_norm_peak": (_i, [_p, _i, _p, _p]),
     "gmg_abs_max_scale": (_i, [_p, _d, _d, _p, _p]),
     "gmg_norm_begin": (_i, [_p]),
     "gmg_norm_end": (_i, [_p, _p]),
@@ -284,6 +285,13 @@ class Context:
         out = np.zeros(2)
         self.check(self.lib.gmg_residual_norm(self.ctx, level, ptr(out)))
         return float(out[0]), float(out[1])
+
+    def residual_parts_peak(self, level=0):
+        """(max|r_int|, max|r_g|, lower bound of max|u| or -1), one pass."""
+        out = np.zeros(2)
+        lb = np.zeros(1)
+        self.check(self.lib.gmg_residual_norm_peak(self.ctx, level, ptr(out), ptr(lb)))
+        return float(out[0]), float(out[1]), float(lb[0])
 
     def abs_max_scale(self, threshold=1e-250, factor=1e250):
         peak = np.zeros(1)

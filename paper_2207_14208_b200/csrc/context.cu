@@ -654,7 +654,7 @@ int op_smooth(gmg_ctx* ctx, DevLevel& l, int count) {
   return 0;
 }
 
-int op_res_int(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
+int op_res_int(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot, unsigned long long* peak = nullptr) {
   Scope s(ctx, slot ? 7 : 2);
   // the norm pass (slot set) only needs the maximum: no residual array writes
   if (l.slab && l.g.d == 3)
@@ -662,7 +662,7 @@ int op_res_int(gmg_ctx* ctx, DevLevel& l, unsigned long long* slot) {
                                     (int)std::max<int64_t>(1, l.slab_lo), (int)std::min<int64_t>(l.g.N - 1, l.slab_hi - 1),
                                     ctx->stream);
   else
-    launch_residual_interior(l.g, l.labels, l.u, l.f, slot ? nullptr : l.rI, slot, ctx->stream);
+    launch_residual_interior(l.g, l.labels, l.u, l.f, slot ? nullptr : l.rI, slot, ctx->stream, slot ? peak : nullptr);
   ctx->launches++;
   return 0;
 }
@@ -1977,11 +1977,12 @@ int gmg_cycle(gmg_ctx* ctx, int ncycles) {
   return 0;
 }
 
-int gmg_residual_norm(gmg_ctx* ctx, int li, double* out) {
+static int residual_norm_impl(gmg_ctx* ctx, int li, double* out, double* peak_lb) {
   if (li < 0 || li >= ctx->nlevels || !ctx->L[li].ready) return fail(ctx, "level not set");
   cudaSetDevice(ctx->device);
   DevLevel& l = ctx->L[li];
   ctx->cur_level = li;
+  if (peak_lb) *peak_lb = -1.0;  // not computed
   if (ctx->norm == 1) {
     // l2: the two sums of squares (the caller takes sqrt(a + b), solver.py:138)
     if (op_res_int(ctx, l, nullptr) || op_res_ghost(ctx, l, nullptr)) return -1;
@@ -1990,20 +1991,28 @@ int gmg_residual_norm(gmg_ctx* ctx, int li, double* out) {
     if (ctx->prof) profile_flush(ctx);
     return 0;
   }
-  GMG_CHECK(ctx, cudaMemsetAsync(ctx->dmax, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  GMG_CHECK(ctx, cudaMemsetAsync(ctx->dmax, 0, 3 * sizeof(unsigned long long), ctx->stream));
   const bool fork = side_begin(ctx);
   if (op_res_ghost(ctx, l, ctx->dmax + 1)) return -1;
   if (side_end(ctx, fork)) return -1;
-  if (op_res_int(ctx, l, ctx->dmax)) return -1;
+  if (op_res_int(ctx, l, ctx->dmax, peak_lb && !l.slab ? ctx->dmax + 2 : nullptr)) return -1;
   if (side_join(ctx, fork)) return -1;
-  GMG_CHECK(ctx, cudaMemcpyAsync(ctx->hmax, ctx->dmax, 2 * sizeof(unsigned long long),
+  GMG_CHECK(ctx, cudaMemcpyAsync(ctx->hmax, ctx->dmax, 3 * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, ctx->stream));
   GMG_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   GMG_CHECK(ctx, cudaGetLastError());
   if (ctx->prof) profile_flush(ctx);
   std::memcpy(out, ctx->hmax, 2 * sizeof(double));
+  if (peak_lb && !l.slab) std::memcpy(peak_lb, ctx->hmax + 2, sizeof(double));
   return 0;
 }
+
+int gmg_residual_norm(gmg_ctx* ctx, int li, double* out) { return residual_norm_impl(ctx, li, out, nullptr); }
+
+int gmg_residual_norm_peak(gmg_ctx* ctx, int li, double* out, double* peak_lb) {
+  return residual_norm_impl(ctx, li, out, peak_lb);
+}
+
 
 // Asynchronous form of residual_norm + the renormalisation check for batched
 // solves (many contexts, one stream each): begin enqueues the inf-norm parts

@@ -114,7 +114,7 @@ void launch_residual_ghost_lex(const GhostArgs& a, const double* wl, const int64
                                unsigned long long* maxbits, int64_t i0, int64_t i1, cudaStream_t st);
 void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,
                               const double* f, double* r, unsigned long long* maxbits,
-                              cudaStream_t st);
+                              cudaStream_t st, unsigned long long* peakbits = nullptr);
 // the same over the internal planes [p_lo, p_hi] only (3-D, z-slab mode)
 void launch_residual_interior_planes(const Geom& g, const uint8_t* labels, const double* u, const double* f, double* r,
                                      unsigned long long* maxbits, int p_lo, int p_hi, cudaStream_t st);

@@ -51,8 +51,9 @@ __global__ void __launch_bounds__(256) residual_interior_kernel(Geom g, const ui
                                                                 const double* __restrict__ u,
                                                                 const double* __restrict__ f,
                                                                 double* __restrict__ r,
-                                                                unsigned long long* maxbits) {
-  double am = 0.0;
+                                                                unsigned long long* maxbits,
+                                                                unsigned long long* peakbits) {
+  double am = 0.0, pm = 0.0;  // pm: max |u| over the internal nodes (norm pass only, see launch_residual_interior)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.nodes;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (lab[i] != INTERNAL) continue;
@@ -62,11 +63,17 @@ __global__ void __launch_bounds__(256) residual_interior_kernel(Geom g, const ui
     else
       s = ((u[i - g.s0] + u[i + g.s0]) + u[i - 1]) + u[i + 1];
     s = s + 0.0;
-    const double v = (f[i] - g.c * u[i]) + div_h2(g, s);
+    const double uc = u[i];
+    const double v = (f[i] - g.c * uc) + div_h2(g, s);
     if (r) r[i] = v;
     am = (__double_as_longlong(fabs(v)) > __double_as_longlong(am)) ? fabs(v) : am;
+    pm = (__double_as_longlong(fabs(uc)) > __double_as_longlong(pm)) ? fabs(uc) : pm;
   }
   block_max_commit(am, maxbits);
+  if (peakbits) {
+    __syncthreads();
+    block_max_commit(pm, peakbits);
+  }
 }
 
 // 3-D version streaming along planes: a CTA owns a 32-column x 8-row tile
@@ -206,7 +213,8 @@ __global__ void __launch_bounds__(RM_TJ * 32) residual_march3_kernel(Geom g, con
                                                                      const double* __restrict__ u,
                                                                      const double* __restrict__ f,
                                                                      double* __restrict__ r,
-                                                                     unsigned long long* maxbits, int p_lo, int p_hi) {
+                                                                     unsigned long long* maxbits, int p_lo, int p_hi,
+                                                                     unsigned long long* peakbits) {
   extern __shared__ __align__(16) unsigned char rm_raw[];
   ResMarchSmem<RM_TJ, RM_S>& S = *reinterpret_cast<ResMarchSmem<RM_TJ, RM_S>*>(rm_raw);
   const int N = (int)g.N;
@@ -289,7 +297,7 @@ __global__ void __launch_bounds__(RM_TJ * 32) residual_march3_kernel(Geom g, con
   for (int p = ib - 1; p <= ib + RM_S - 2; ++p) fetch(p);
   const int tj = tid >> 5, lane = tid & 31;
   const int j = j0 + tj;
-  double am = 0.0;
+  double am = 0.0, pm = 0.0;
   for (int i = ib; i <= ie; ++i) {
     cpa_wait<RM_S - 3>();  // planes <= i+1 have landed
     __syncthreads();
@@ -308,16 +316,22 @@ __global__ void __launch_bounds__(RM_TJ * 32) residual_march3_kernel(Geom g, con
       const double v = (S.f[sc][tj][kk] - g.c * uc) + div_h2(g, s);
       if (WRITE) r[((int64_t)i * g.n + j) * g.P + k + OFF] = v;
       am = (__double_as_longlong(fabs(v)) > __double_as_longlong(am)) ? fabs(v) : am;
+      if (!WRITE) pm = (__double_as_longlong(fabs(uc)) > __double_as_longlong(pm)) ? fabs(uc) : pm;
     }
     __syncthreads();  // slot of plane i-1 is refilled next
     fetch(i + RM_S - 1);
   }
   cpa_wait<0>();
   block_max_commit(am, maxbits);
+  if (!WRITE && peakbits) {
+    __syncthreads();
+    block_max_commit(pm, peakbits);
+  }
 }
 
 static void launch_residual_march(const Geom& g, const uint8_t* labels, const double* u, const double* f, double* r,
-                                  unsigned long long* maxbits, int p_lo, int p_hi, cudaStream_t st);
+                                  unsigned long long* maxbits, int p_lo, int p_hi, cudaStream_t st,
+                                  unsigned long long* peakbits = nullptr);
 
 void launch_residual_interior_planes(const Geom& g, const uint8_t* labels, const double* u, const double* f, double* r,
                                      unsigned long long* maxbits, int p_lo, int p_hi, cudaStream_t st) {
@@ -326,9 +340,12 @@ void launch_residual_interior_planes(const Geom& g, const uint8_t* labels, const
 
 void launch_residual_interior(const Geom& g, const uint8_t* labels, const double* u,
                               const double* f, double* r, unsigned long long* maxbits,
-                              cudaStream_t st) {
+                              cudaStream_t st, unsigned long long* peakbits) {
+  // peakbits (norm pass, r == nullptr): also max |u| over the internal nodes -- a lower bound of max |u| that
+  // lets the caller skip the full-array pass of the renormalisation check (solver.py:241-245) when it is
+  // already above the threshold
   if (g.d == 3 && !getenv("GMG_RES_ROWS")) {
-    launch_residual_march(g, labels, u, f, r, maxbits, 1, (int)g.N - 1, st);
+    launch_residual_march(g, labels, u, f, r, maxbits, 1, (int)g.N - 1, st, peakbits);
   } else if (g.d == 3 && getenv("GMG_RES_STREAM")) {
     dim3 grid((unsigned)((g.N - 1 + RT_K - 1) / RT_K), (unsigned)((g.N - 1 + RT_J - 1) / RT_J));
     residual_stream3_kernel<<<grid, 256, 0, st>>>(g, labels, u, f, r, maxbits);
@@ -340,12 +357,13 @@ void launch_residual_interior(const Geom& g, const uint8_t* labels, const double
     else
       residual_rows3_kernel<false><<<blocks, 128, 0, st>>>(g, labels, u, f, r, maxbits);
   } else {
-    residual_interior_kernel<2><<<grid_for(g.nodes, 256), 256, 0, st>>>(g, labels, u, f, r, maxbits);
+    residual_interior_kernel<2><<<grid_for(g.nodes, 256), 256, 0, st>>>(g, labels, u, f, r, maxbits, r ? nullptr : peakbits);
   }
 }
 
 static void launch_residual_march(const Geom& g, const uint8_t* labels, const double* u, const double* f, double* r,
-                                  unsigned long long* maxbits, int p_lo, int p_hi, cudaStream_t st) {
+                                  unsigned long long* maxbits, int p_lo, int p_hi, cudaStream_t st,
+                                  unsigned long long* peakbits) {
   {
     // 8-row x 64-column tiles; ring of 4 plane slots (5 CTAs per SM) on the
     // largest grids, 5 slots (4 CTAs per SM) below N = 512 (measured per level)
@@ -369,14 +387,14 @@ static void launch_residual_march(const Geom& g, const uint8_t* labels, const do
     dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)segs);
     if (big) {
       if (r)
-        residual_march3_kernel<true, 8, 4><<<grid, 256, sizeof(ResMarchSmem<8, 4>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi);
+        residual_march3_kernel<true, 8, 4><<<grid, 256, sizeof(ResMarchSmem<8, 4>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi, peakbits);
       else
-        residual_march3_kernel<false, 8, 4><<<grid, 256, sizeof(ResMarchSmem<8, 4>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi);
+        residual_march3_kernel<false, 8, 4><<<grid, 256, sizeof(ResMarchSmem<8, 4>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi, peakbits);
     } else {
       if (r)
-        residual_march3_kernel<true, 8, 5><<<grid, 256, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi);
+        residual_march3_kernel<true, 8, 5><<<grid, 256, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi, peakbits);
       else
-        residual_march3_kernel<false, 8, 5><<<grid, 256, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi);
+        residual_march3_kernel<false, 8, 5><<<grid, 256, sizeof(ResMarchSmem<8, 5>), st>>>(g, labels, u, f, r, maxbits, p_lo, p_hi, peakbits);
     }
   }
 }

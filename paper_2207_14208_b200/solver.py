@@ -288,6 +288,7 @@ class MultigridSolver(CycleDriver):
             self.ctx.set_vector(0, _lib.G, g_fine)
 
     def _put_u(self, u):
+        self._peak_lb = None
         self.ctx.set_vector(0, _lib.U, u)
 
     def _get_u(self):
@@ -313,10 +314,14 @@ class MultigridSolver(CycleDriver):
         return True
 
     def _run_cycle(self):
+        self._peak_lb = None
         self.ctx.cycle(1)
 
     def _residual_norm(self):
-        m_int, m_g = self.ctx.residual_parts(0)
+        # the norm pass also returns max|u| over the internal nodes: when that is already above the
+        # renormalisation threshold, _abs_max_scale (called right after, u unchanged) has its answer
+        m_int, m_g, lb = self.ctx.residual_parts_peak(0)
+        self._peak_lb = lb
         if self.cycle_cfg.norm == NORM_L2:
             # device sums of squares, NumPy's pairwise order (solver.py:138)
             return math.sqrt(float(m_int + m_g))
@@ -327,6 +332,12 @@ class MultigridSolver(CycleDriver):
         return m
 
     def _abs_max_scale(self):
+        """(peak, scaled) of the renormalisation guard (reference solver.py:239-243).  peak is max|u|, or,
+        when the preceding norm pass already found an internal |u| >= the threshold, that lower bound
+        (the guard's outcome is the same: no rescaling)."""
+        lb, self._peak_lb = getattr(self, "_peak_lb", None), None
+        if lb is not None and lb >= 1e-250:
+            return lb, False
         return self.ctx.abs_max_scale(1e-250, 1e250)
 
 

@@ -359,3 +359,37 @@ def test_gs_chain_matches_stream_kernel(case, gpu_available, monkeypatch):
         ctx.close()
     assert np.array_equal(out[0].view(np.uint64), out[1].view(np.uint64))
     assert np.array_equal(out[0].view(np.uint64), out[2].view(np.uint64))
+
+
+@pytest.mark.parametrize("case", ["ball32", "pores64", "disk64"])
+def test_norm_pass_peak_lower_bound(case, gpu_available):
+    """gmg_residual_norm_peak: the same two maxima as gmg_residual_norm and max|u| over the internal nodes,
+    and the solve loop's renormalisation guard (reference solver.py:239-243) still rescales a tiny iterate
+    when that bound is below the threshold."""
+    from paper_2207_14208_b200 import configs as CF
+    from paper_2207_14208_b200.cycle import CycleDriver
+    from paper_2207_14208_b200.transfer import build_hierarchy
+
+    setup = {"ball32": lambda: CF.config_ball(32, cycles=3), "pores64": lambda: CF.config_pores(N=64, cycles=3),
+             "disk64": lambda: CF.config_disk(64, cycles=3)}[case]()
+    levels = build_hierarchy(setup.grid, setup.phi, setup.faces, max_levels=setup.cycle.max_levels,
+                             coarsest_min=setup.coarsest_min)
+    plans, f, g, e = CycleDriver.problem_data(levels, setup.spec, setup.smoother, setup.default_variant)
+    dev = MultigridSolver.from_plans(plans, f, g, e, setup.smoother, setup.cycle)
+    p = plans[0]
+    rng = np.random.default_rng(5)
+    u = rng.standard_normal(p.n_nodes)
+    dev._set_data(dev.f_fine, dev.g_fine)
+    dev._put_u(u)
+    a = dev.ctx.residual_parts(0)
+    b = dev.ctx.residual_parts_peak(0)
+    assert a == b[:2]
+    assert b[2] == np.abs(u[p.labels == 0]).max()
+    assert dev._residual_norm() == max(a) and dev._abs_max_scale() == (b[2], False)
+    # tiny iterate: the bound is below the threshold, the exact pass runs and rescales
+    dev._put_u(u * 1e-255)
+    dev._residual_norm()
+    peak, scaled = dev._abs_max_scale()
+    assert scaled and peak == np.abs(u * 1e-255).max()
+    got = dev._get_u()
+    assert np.array_equal(got, (u * 1e-255) * 1e250)
