@@ -40,7 +40,6 @@ unsigned grid_for(int64_t n, int threads, int64_t cap = 148 * 16) {
   return (unsigned)b;
 }
 
-constexpr int IC = 2;  // columns per thread of the row kernels
 
 }  // namespace
 
@@ -74,106 +73,6 @@ __global__ void __launch_bounds__(256) residual_interior_kernel(Geom g, const ui
     __syncthreads();
     block_max_commit(pm, peakbits);
   }
-}
-
-// 3-D version streaming along planes: a CTA owns a 32-column x 8-row tile
-// and marches over the planes, holding the planes below/above its own nodes
-// in registers and the current plane's tile (+1 halo) in shared memory, so u
-// is read from HBM about once.  Same arithmetic order as above.  With
-// r == nullptr only the maximum is produced (the residual-norm pass).
-constexpr int RT_J = 8, RT_K = 32;
-__global__ void __launch_bounds__(256) residual_stream3_kernel(Geom g, const uint8_t* __restrict__ lab,
-                                                               const double* __restrict__ u,
-                                                               const double* __restrict__ f,
-                                                               double* __restrict__ r,
-                                                               unsigned long long* maxbits) {
-  __shared__ double tile[RT_J + 2][RT_K + 2];
-  const int N = (int)g.N;
-  const int tk = threadIdx.x & 31, tj = threadIdx.x >> 5;
-  const int k = 1 + (int)blockIdx.x * RT_K + tk;   // column
-  const int j = 1 + (int)blockIdx.y * RT_J + tj;   // row
-  const bool mine = k <= N - 1 && j <= N - 1;
-  const int kc = min(k, N), jc = min(j, N);        // clamped (in-grid) position
-  const int64_t col = (int64_t)kc + OFF;
-  auto at = [&](int i, int jj) -> int64_t { return ((int64_t)i * g.n + jj) * g.P; };
-  // halo cells of the tile: 2 x RT_K row cells + 2 x (RT_J + 2) column cells
-  auto load_tile = [&](int i) {
-    tile[tj + 1][tk + 1] = u[at(i, jc) + col];
-    const int t = threadIdx.x;
-    if (t < 2 * RT_K) {  // rows j0-1 and j0+RT_J
-      const int hj = t < RT_K ? (int)blockIdx.y * RT_J : min((int)blockIdx.y * RT_J + RT_J + 1, N);
-      const int hk = min(1 + (int)blockIdx.x * RT_K + (t & (RT_K - 1)), N);
-      tile[t < RT_K ? 0 : RT_J + 1][(t & (RT_K - 1)) + 1] = u[at(i, hj) + hk + OFF];
-    } else if (t < 2 * RT_K + 2 * (RT_J + 2)) {  // columns k0-1 and k0+RT_K
-      const int q = t - 2 * RT_K, side = q / (RT_J + 2), rr = q % (RT_J + 2);
-      const int hj = min((int)blockIdx.y * RT_J + rr, N);
-      const int hk = side == 0 ? (int)blockIdx.x * RT_K : min((int)blockIdx.x * RT_K + RT_K + 1, N);
-      tile[rr][side == 0 ? 0 : RT_K + 1] = u[at(i, hj) + hk + OFF];
-    }
-  };
-  double um = u[at(0, jc) + col];
-  load_tile(1);
-  __syncthreads();
-  double uc = tile[tj + 1][tk + 1];
-  double am = 0.0;
-  for (int i = 1; i <= N - 1; ++i) {
-    const double up = u[at(i + 1, jc) + col];
-    const int64_t pos = at(i, jc) + col;
-    if (mine && lab[pos] == INTERNAL) {
-      double s = ((((um + up) + tile[tj][tk + 1]) + tile[tj + 2][tk + 1]) + tile[tj + 1][tk]) + tile[tj + 1][tk + 2];
-      s = s + 0.0;
-      const double v = (f[pos] - g.c * uc) + s / g.h2;
-      if (r) r[pos] = v;
-      am = (__double_as_longlong(fabs(v)) > __double_as_longlong(am)) ? fabs(v) : am;
-    }
-    __syncthreads();
-    if (i < N - 1) load_tile(i + 1);
-    __syncthreads();
-    um = uc;
-    uc = up;
-  }
-  block_max_commit(am, maxbits);
-}
-
-// 3-D row version: interior rows only (every stencil access in bounds), IC
-// columns per thread with all loads issued first.
-template <bool WRITE>
-__global__ void __launch_bounds__(128) residual_rows3_kernel(Geom g, const uint8_t* __restrict__ lab,
-                                                             const double* __restrict__ u,
-                                                             const double* __restrict__ f,
-                                                             double* __restrict__ r,
-                                                             unsigned long long* maxbits) {
-  const int N = (int)g.N;
-  const int inner = N - 1;
-  const int64_t nrows = (int64_t)inner * inner;
-  double am = 0.0;
-  for (int64_t rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
-    const int64_t i = rr / inner + 1, j = rr % inner + 1;
-    const int64_t base = (i * g.n + j) * g.P + OFF;
-    for (int k0 = 1 + threadIdx.x; k0 <= N - 1; k0 += IC * blockDim.x) {
-      double s[IC], uc[IC], fv[IC];
-      uint8_t L[IC];
-#pragma unroll
-      for (int q = 0; q < IC; ++q) {
-        const int kk = k0 + q * (int)blockDim.x;
-        const int kc = kk <= N - 1 ? kk : N - 1;
-        const int64_t p = base + kc;
-        L[q] = kk <= N - 1 ? lab[p] : (uint8_t)PAD;  // out of the row: never written
-        uc[q] = u[p];
-        fv[q] = f[p];
-        s[q] = ((((u[p - g.s0] + u[p + g.s0]) + u[p - g.s1]) + u[p + g.s1]) + u[p - 1]) + u[p + 1];
-      }
-#pragma unroll
-      for (int q = 0; q < IC; ++q) {
-        if (L[q] != INTERNAL) continue;
-        const double sv = s[q] + 0.0;
-        const double v = (fv[q] - g.c * uc[q]) + div_h2(g, sv);
-        if (WRITE) r[base + k0 + q * (int)blockDim.x] = v;
-        am = (__double_as_longlong(fabs(v)) > __double_as_longlong(am)) ? fabs(v) : am;
-      }
-    }
-  }
-  block_max_commit(am, maxbits);
 }
 
 // 3-D plane-marching version (production): a CTA owns RM_TJ rows x RM_TK
@@ -344,21 +243,10 @@ void launch_residual_interior(const Geom& g, const uint8_t* labels, const double
   // peakbits (norm pass, r == nullptr): also max |u| over the internal nodes -- a lower bound of max |u| that
   // lets the caller skip the full-array pass of the renormalisation check (solver.py:241-245) when it is
   // already above the threshold
-  if (g.d == 3 && !getenv("GMG_RES_ROWS")) {
+  if (g.d == 3)
     launch_residual_march(g, labels, u, f, r, maxbits, 1, (int)g.N - 1, st, peakbits);
-  } else if (g.d == 3 && getenv("GMG_RES_STREAM")) {
-    dim3 grid((unsigned)((g.N - 1 + RT_K - 1) / RT_K), (unsigned)((g.N - 1 + RT_J - 1) / RT_J));
-    residual_stream3_kernel<<<grid, 256, 0, st>>>(g, labels, u, f, r, maxbits);
-  } else if (g.d == 3) {
-    const int64_t nrows = (g.N - 1) * (g.N - 1);
-    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 16));
-    if (r)
-      residual_rows3_kernel<true><<<blocks, 128, 0, st>>>(g, labels, u, f, r, maxbits);
-    else
-      residual_rows3_kernel<false><<<blocks, 128, 0, st>>>(g, labels, u, f, r, maxbits);
-  } else {
+  else
     residual_interior_kernel<2><<<grid_for(g.nodes, 256), 256, 0, st>>>(g, labels, u, f, r, maxbits, r ? nullptr : peakbits);
-  }
 }
 
 static void launch_residual_march(const Geom& g, const uint8_t* labels, const double* u, const double* f, double* r,
@@ -500,63 +388,6 @@ __global__ void __launch_bounds__(256, 3) restrict_interior_kernel(Geom gf, cons
         for (int e = 0; e < M; ++e) p[e] = fw_w<D>(e) * p[e];
       }
       f_c[ic] = np_sum<M>(p);
-    }
-  }
-}
-
-// 3-D pair variant: a thread takes coarse columns K, K+1 (K odd) of a row;
-// per fine (plane, row) of their 3 x 3 block rows it loads the five fine
-// columns 2K-1 .. 2K+3 as two 16-byte loads and one 8-byte load (the nodes
-// share column 2K+1), the two masks as one 8-byte load.  Same weights and
-// summation order as restrict_interior_kernel.
-__global__ void __launch_bounds__(128) restrict_pair3_kernel(Geom gf, const double* __restrict__ r_f, Geom gc,
-                                                              const uint32_t* __restrict__ rmask,
-                                                              double* __restrict__ f_c) {
-  const int nc = (int)gc.n;
-  const int inner = nc - 2;
-  const int64_t nrows = (int64_t)inner * inner;
-  const int npairs = (inner + 1) / 2;
-  for (int64_t rr = blockIdx.x; rr < nrows; rr += gridDim.x) {
-    const int I = (int)(rr / inner) + 1, J = (int)(rr % inner) + 1;
-    const int64_t crow = (int64_t)I * nc + J;
-    const int64_t frow = (int64_t)(2 * I) * gf.n + 2 * J;
-    for (int t = threadIdx.x; t < npairs; t += blockDim.x) {
-      const int K = 1 + 2 * t;
-      const bool two = K + 1 <= nc - 2;
-      const int64_t ic = crow * gc.P + K + OFF;  // even position: 8-byte aligned pair of masks
-      uint32_t m0, m1;
-      if (two) {
-        const uint2 mm = *reinterpret_cast<const uint2*>(rmask + ic);
-        m0 = mm.x, m1 = mm.y;
-      } else {
-        m0 = rmask[ic], m1 = 0u;
-      }
-      if (!((m0 | m1) & RM_COARSE)) continue;
-      double p0[27], p1[27];
-#pragma unroll
-      for (int pr = 0; pr < 9; ++pr) {  // (plane, row) of the block: e = 3 pr + column
-        const int dp = pr / 3 - 1, dr = pr % 3 - 1;
-        const double* rc = r_f + (frow + (int64_t)dp * gf.n + dr) * gf.P + 2 * K - 1 + OFF;  // column 2K-1
-        const double2 a = *reinterpret_cast<const double2*>(rc);
-        const double2 b = *reinterpret_cast<const double2*>(rc + 2);
-        const double c = two ? rc[4] : 0.0;
-        p0[3 * pr] = a.x, p0[3 * pr + 1] = a.y, p0[3 * pr + 2] = b.x;
-        p1[3 * pr] = b.x, p1[3 * pr + 1] = b.y, p1[3 * pr + 2] = c;
-      }
-      auto finish = [&](uint32_t m, double(&p)[27]) -> double {
-        if (m & RM_MIXED) {
-          const double dc = (double)__popc(m & ((1u << 27) - 1u));
-          const double w1 = 1.0 / dc;
-#pragma unroll
-          for (int e = 0; e < 27; ++e) p[e] = (((m >> e) & 1u) ? w1 : 0.0) * p[e];  // == (bit ? 1 : 0) / dc * p
-        } else {
-#pragma unroll
-          for (int e = 0; e < 27; ++e) p[e] = fw_w<3>(e) * p[e];
-        }
-        return np_sum<27>(p);
-      };
-      if (m0 & RM_COARSE) f_c[ic] = finish(m0, p0);
-      if (two && (m1 & RM_COARSE)) f_c[ic + 1] = finish(m1, p1);
     }
   }
 }
@@ -772,15 +603,7 @@ void launch_restrict_interior(const Geom& gf, const double* r_f, const Geom& gc,
   const int64_t inner = gc.n - 2;
   const int64_t nrows = gf.d == 3 ? inner * inner : inner;
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 8));
-  static int pair = -1;
-  if (pair < 0) {
-    const char* env = getenv("GMG_RESTRICT_PAIR");
-    pair = env ? atoi(env) : 0;  // measured slower (371 vs 323 us at 512^3)
-  }
-  if (gf.d == 3 && pair) {
-    const unsigned b2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 16));
-    restrict_pair3_kernel<<<b2, 128, 0, st>>>(gf, r_f, gc, rmask, f_c);
-  } else if (gf.d == 3)
+  if (gf.d == 3)
     restrict_interior_kernel<3><<<blocks, 256, 0, st>>>(gf, r_f, gc, rmask, f_c);
   else
     restrict_interior_kernel<2><<<blocks, 256, 0, st>>>(gf, r_f, gc, rmask, f_c);
@@ -789,87 +612,12 @@ void launch_restrict_interior(const Geom& gf, const double* r_f, const Geom& gc,
 // ErrorInterpolation + correction (transfer.py:124-151, solver.py:198):
 // u += sum_c w_c e[src_c] on internal and ghost fine nodes; corner c of
 // {0,1}^D in C order, w_c = prod_k (odd_k ? 1/2 : [c_k == 0]).
-// The padded fine array is walked as 16-byte pairs of positions (2m, 2m+1)
-// -- fine columns k = 2m-3 (odd) and 2m-2 (even), which share the coarse
-// columns m-2 and m-1 -- so u moves as one vector load/store and the labels
-// as one 2-byte load; each thread takes PPT pairs a grid stride apart with
-// all their loads issued before any arithmetic.  Zero-weight corners are
-// still multiplied and summed, like the reference's dense 2^D product.
-constexpr int PPT = 2;  // pairs per thread
-
-template <int D>
-__global__ void __launch_bounds__(256, 4) interp_add_kernel(Geom gf, const uint8_t* __restrict__ lab_f,
-                                                            double* __restrict__ u, Geom gc,
-                                                            const double* __restrict__ e) {
-  constexpr int NC = 1 << D;
-  constexpr int NR = D == 3 ? 4 : 2;  // corner rows (c0, c1)
-  const int nf = (int)gf.n;
-  const int hp = (int)(gf.P >> 1);  // pairs per row
-  const int npairs = (int)(gf.rows * hp);
-  const int stride = gridDim.x * blockDim.x;
-  for (int q0 = blockIdx.x * blockDim.x + threadIdx.x; q0 < npairs; q0 += PPT * stride) {
-    double2 uv[PPT];
-    uint16_t L2v[PPT];
-    double ea[PPT][NR], eb[PPT][NR];
-    int oij[PPT];
-    // loads: u pair, labels, coarse columns m-2 / m-1 of every corner row
-#pragma unroll
-    for (int t = 0; t < PPT; ++t) {
-      const int q = min(q0 + t * stride, npairs - 1);
-      const int row = q / hp, m = q - row * hp;
-      const int ii = D == 3 ? row / nf : 0;
-      const int jj = D == 3 ? row - ii * nf : row;
-      uv[t] = reinterpret_cast<const double2*>(u)[q];
-      L2v[t] = reinterpret_cast<const uint16_t*>(lab_f)[q];
-      const int oi = ii & 1, oj = jj & 1;
-      oij[t] = oi * 2 + oj;
-      const int hi = ii >> 1, hj = jj >> 1;
-      // (clamped inside the padded row for pad pairs)
-      const int cm = max(m - 2, 0) + (int)OFF, cn = max(m - 1, 0) + (int)OFF;
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const int c0 = D == 3 ? r >> 1 : 0, c1 = r & 1;
-        const int ri = hi + (oi ? c0 : 0), rj = hj + (oj ? c1 : 0);
-        const double* er = e + (D == 3 ? ((int64_t)ri * gc.n + rj) * gc.P : (int64_t)rj * gc.P);
-        ea[t][r] = er[cm];
-        eb[t][r] = er[cn];
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < PPT; ++t) {
-      const int q = q0 + t * stride;
-      if (q >= npairs) continue;
-      const uint8_t la = (uint8_t)(L2v[t] & 0xFF), lb = (uint8_t)(L2v[t] >> 8);
-      const bool wa = la == INTERNAL || la == GHOST, wb = lb == INTERNAL || lb == GHOST;
-      if (!wa && !wb) continue;
-      const int oi = oij[t] >> 1, oj = oij[t] & 1;
-      double pa[NC], pb[NC];
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const int c0 = D == 3 ? r >> 1 : 0, c1 = r & 1;
-        const double wi = oi ? 0.5 : (c0 == 0 ? 1.0 : 0.0);
-        const double wj = oj ? 0.5 : (c1 == 0 ? 1.0 : 0.0);
-        const double wr = D == 3 ? (1.0 * wi) * wj : 1.0 * wj;
-        // odd column k = 2m-3: hk = m-2, col1 = m-1, weights (1/2, 1/2);
-        // even column k = 2m-2: hk = col1 = m-1, weights (1, 0)
-        pa[2 * r] = (wr * 0.5) * ea[t][r];
-        pa[2 * r + 1] = (wr * 0.5) * eb[t][r];
-        pb[2 * r] = (wr * 1.0) * eb[t][r];
-        pb[2 * r + 1] = (wr * 0.0) * eb[t][r];
-      }
-      double2 o = uv[t];
-      if (wa) o.x = uv[t].x + np_sum<NC>(pa);
-      if (wb) o.y = uv[t].y + np_sum<NC>(pb);
-      reinterpret_cast<double2*>(u)[q] = o;
-    }
-  }
-}
-
-// Quad variant: a thread takes padded positions 4q .. 4q+3 (fine columns
-// 4q-3 .. 4q, one 32-byte-aligned group): u as two 16-byte loads, the labels as
-// one 4-byte load, and per corner row only the three coarse columns 2q-2 .. 2q
-// the four nodes share (12 coarse loads for 4 nodes instead of 16).  Same
-// products and sums as interp_add_kernel.
+// A thread takes padded positions 4q .. 4q+3 of the fine array (fine columns
+// 4q-3 .. 4q, one 32-byte-aligned group): u as two 16-byte loads, the labels
+// as one 4-byte load, and per corner row only the three coarse columns
+// 2q-2 .. 2q the four nodes share (12 coarse loads for 4 nodes instead of
+// 16).  Zero-weight corners are still multiplied and summed, like the
+// reference's dense 2^D product.
 template <int D>
 __global__ void __launch_bounds__(256, 4) interp_add4_kernel(Geom gf, const uint8_t* __restrict__ lab_f,
                                                           double* __restrict__ u, Geom gc,
@@ -938,26 +686,12 @@ __global__ void __launch_bounds__(256, 4) interp_add4_kernel(Geom gf, const uint
 
 void launch_interp_add(const Geom& gf, const uint8_t* lab_f, double* u_f, const Geom& gc,
                        const double* e_c, cudaStream_t st) {
-  static int quad = -1;
-  if (quad < 0) {
-    const char* env = getenv("GMG_INTERP4");
-    quad = env ? atoi(env) : 1;
-  }
-  if (quad) {
-    const int64_t nq = gf.rows * (gf.P / 4);
-    const unsigned blocks = grid_for(nq, 256, 148 * 8);
-    if (gf.d == 3)
-      interp_add4_kernel<3><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
-    else
-      interp_add4_kernel<2><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
-    return;
-  }
-  const int64_t npairs = gf.rows * (gf.P / 2);
-  const unsigned blocks = grid_for((npairs + PPT - 1) / PPT, 256, 148 * 8);
+  const int64_t nq = gf.rows * (gf.P / 4);
+  const unsigned blocks = grid_for(nq, 256, 148 * 8);
   if (gf.d == 3)
-    interp_add_kernel<3><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
+    interp_add4_kernel<3><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
   else
-    interp_add_kernel<2><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
+    interp_add4_kernel<2><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
 }
 
 // Band BFS group (transfer.py:245-246): x_i = (sum_k x[nbr_k] * mask_k) /
