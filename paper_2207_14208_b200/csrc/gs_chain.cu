@@ -12,40 +12,41 @@
 //
 // Tasks.  A task is a 16-column chunk c (columns k0 = 1+16c .. k0+15) x a
 // block b of 8 rows (rowbase = 1 + 8b ..) x the planes [P0, P1] that hold
-// internal nodes of the task.  ONE warp computes a task: lane (h, j) owns
-// column k0+j and the four rows ("chains") rowbase + 4h + i, i = 0..3; with
-// I = 4h + i, chain I of lane j relaxes plane p = P0 + t - j - I at step t.
-// Then every NEW operand of a node was produced one step earlier and is
-// still in a register -- the plane below by the chain itself, the row above
-// by the lane's chain I-1 (for I = 4: lane j of the other half-warp, one
-// shuffle), the left neighbour by lane j-1's chain I (one shuffle) -- and
-// every OLD operand is read before the step that overwrites it.  The
-// loop-carried dependency of a step is seven fp64 operations per chain with
-// four independent chains per lane to fill the pipeline; there is no
-// shared-memory hand-off and no barrier inside a task.  A task runs
+// internal nodes of the task.  One CTA of five warps runs a task.  Two
+// compute warps: warp A owns columns k0 .. k0+7, warp B columns k0+8 ..
+// k0+15 and runs SHB = 8 steps behind A; lane (g, j) of a warp owns its
+// column j and the two rows ("chains") rowbase + 2g + i, i = 0, 1, and chain
+// i relaxes plane p = P0 + t - j - 2g - i (- SHB for B) at step t.  Then
+// every NEW operand of a node was produced one step earlier and is still in a
+// register -- the plane below by the chain itself, the row above by the
+// lane's chain 0 (for chain 0: row group g-1's chain 1, one shuffle), the left
+// neighbour by lane j-1 (one shuffle; B's lane 0 reads A's column 7 from the
+// ring) -- and every OLD operand is read before the step that overwrites it.
+// The loop-carried dependency of a step is a shuffle and seven fp64
+// operations; there is no barrier inside a task.  A task runs
 // (P1 - P0) + 23 steps.
 //
-// Data.  Groups of G planes of a task are filled by two TMA boxes (u rows
-// rowbase-1 .. rowbase+8 over columns k0-2 .. k0+17, and f) into a ring of NS
-// plane slots; the warp updates u in place in the ring (for the writer), a
-// writer warp copies finished planes back to HBM.  Lane j at plane p - j
-// reads its tile at column 2+j: the 16 lanes of a half-warp hit 16 distinct
-// bank pairs (plane stride 1600 B).  Which nodes are internal comes from a
-// plane-transposed bit mask (word (p >> 5, r, k), bit p & 31) that each lane
-// reads from global memory once per 32 steps and chain.
+// Data.  A loader warp (one lane) fills groups of G planes of the task with
+// two TMA boxes (u rows rowbase-1 .. rowbase+8 over columns k0-2 .. k0+17 -- a
+// box starts on a 16-byte boundary -- and f) into a ring of NS plane slots;
+// the compute warps update u in place in the ring, a writer warp copies
+// finished planes back to HBM and pushes the last row / column to the
+// downstream tasks.  Which nodes are internal comes from a plane-transposed
+// bit mask (word (p >> 5, r, k), bit p & 31) that each lane reads from global
+// memory once per 32 steps and chain, all lanes at the same steps.
 //
 // Neighbour tasks.  The row above the block (task (c, b-1)) and the column
 // left of the chunk (task (c-1, b)) arrive as per-node cells (value, tag):
-// the upstream task stores each final value of its last row / column with
-// one 16-byte store as soon as it is computed, and a cell warp here polls
-// them per lane (L2), puts them into the ring's halo row / column and raises
-// per-lane ready counters.  The hand-off lags by 8 steps (rows) / 15 steps
-// (columns) plus an L2 round trip.  Tags carry a per-level sweep sequence
-// number (advanced by the last CTA of each sweep), so cells never need
-// clearing.  Tasks are claimed by ticket in an order that puts every task
-// after its two upstream tasks, so the sweep cannot deadlock for any grid
-// size; planes without internal nodes are forwarded to the downstream cells
-// at task start.
+// the upstream writer stores each final value of its last row / column with
+// one 16-byte store, and the cells warp here polls them per lane (L2), puts
+// them into the ring's halo row / column and raises per-column / per-row
+// ready counters.  The hand-off lags by 7 steps (rows) / 15 steps (columns)
+// plus the writer's lag and an L2 round trip.  Tags carry a per-level sweep
+// sequence number (advanced by the last CTA of each sweep), so cells never
+// need clearing.  Tasks are claimed by ticket in an order that puts every
+// task after its two upstream tasks, so the sweep cannot deadlock for any
+// grid size; planes without internal nodes are forwarded to the downstream
+// cells in batches before and after the task's own planes.
 //
 // Arithmetic per node is the reference's: ((h^2 f + 0) + ((((pb + pa) + ra)
 // + rb) + lf) + rt)) * (1 / denom) with pb, pa, ra, rb, lf, rt the plane
