@@ -113,33 +113,45 @@ class ClockSampler:
         self._t = None
         self._nvml = None
 
-    def _run(self):
+    def _open(self):
+        # NVML is opened before the timed region (the first nvmlInit takes longer than a short region)
         try:
             import pynvml as N
             N.nvmlInit()
-            h = N.nvmlDeviceGetHandleByIndex(self.index)
-            self._max = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            self._N = N
+            self._h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self._max = N.nvmlDeviceGetMaxClockInfo(self._h, N.NVML_CLOCK_SM)
         except Exception as exc:  # no NVML: record why
             self._err = repr(exc)
-            return
+            self._N = None
+
+    def _sample(self):
+        try:
+            sm = self._N.nvmlDeviceGetClockInfo(self._h, self._N.NVML_CLOCK_SM)
+            rs = self._N.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            self.samples.append((sm, rs))
+        except Exception:
+            pass
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
-                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, rs))
-            except Exception:
-                pass
+            self._sample()
             self._stop.wait(self.period)
 
     def __enter__(self):
         self._err = None
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        self._open()
+        if self._N is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t is not None:
+            self._t.join(timeout=10)
+        if self._N is not None and not self.samples:
+            self._sample()  # a region shorter than the thread's start-up: the clocks right at its end
 
     def summary(self):
         if not self.samples:
