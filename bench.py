@@ -226,7 +226,8 @@ def run_reference(args, rank):
     line = {
         "impl": "reference", "metric": "fine-grid DOF*V-cycles/s (fp64)", "value": value,
         "unit": "DOF*cycles/s", "n_gpus": args.gpus, "steps": done, "steps_requested": args.steps,
-        "warmup": min(args.warmup, 1), "ms_per_step": dt / done * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": min(args.warmup, 1), "ms_per_step": dt / done * 1e3, "higher_is_better": True,
+        "scaling": "strong" if args.gpus > 1 else "weak",  # as the b200 arm: N ranks share the one problem
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": setup.name, "N": setup.grid.N, "levels": len(plans), "dof": dof,
                    "cycle": "V(2,1)", "parallelism": "cpu-1thread"},
