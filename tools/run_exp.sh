@@ -1,1 +1,1 @@
-for v in g4 g6; do echo "== $v"; GMG_LIB_OVERRIDE=build/exp_$v/libghostmg_b200.so timeout 600 python tools/gs_time.py c4:512 10 2>&1 | head -3; GMG_LIB_OVERRIDE=build/exp_$v/libghostmg_b200.so CMP_MODE=01 SWEEPS=2 timeout 600 python tools/gs_cmp.py c4:512 2>&1 | head -1; done
+for v in pfd19 pfd18 pfd16 pfd13; do echo "== $v"; GMG_LIB_OVERRIDE=build/exp_$v/libghostmg_b200.so timeout 600 python tools/gs_time.py c4:512 10 2>&1 | head -2; done
