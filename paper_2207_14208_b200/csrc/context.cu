@@ -1430,7 +1430,7 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
   l.chain_gs = false;
   if (d == 3 && N >= 64 && ctx->gs_chain && chain_ok && !empty_im.empty()) {
     // gs_chain.cu tasks: 16-column chunk c x block of 8 rows; per task the
-    // planes that hold internal nodes; tickets ordered by 4c + 3b (every task
+    // planes that hold internal nodes; tickets ordered by 2c + 3b (every task
     // after its two upstream tasks; a column hop lags ~4/3 of a row hop)
     const int R = GS_CHAIN_ROWS, W = GS_CHAIN_COLS;
     const int C = (int)((N - 1 + W - 1) / W), Bn = (int)((N - 1 + R - 1) / R);
@@ -1451,8 +1451,16 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     rt.reserve((size_t)C * Bn);
     for (int c = 0; c < C; ++c)
       for (int b = 0; b < Bn; ++b) rt.push_back(make_int2(c, b));
-    std::stable_sort(rt.begin(), rt.end(), [](const int2& x, const int2& y) {
-      const int kx = 4 * x.x + 3 * x.y, ky = 4 * y.x + 3 * y.y;
+    // Ticket order: by wc * c + wb * b, which puts every task after its two upstream tasks for any positive
+    // weights.  The weights decide which ~2 * SMs tasks are resident together; measured at 512^3 (sweep, us):
+    // 4:3 1695, 1:1 1817, 2:1 1749, 3:4 1605, 2:3 1586, 4:7 1594, 5:9 1599, 1:2 1635, 1:3 1768, 1:32 2176;
+    // striped orders (blocks of 8-32 rows or columns first) 1690-2360.  256^3: 509 (4:3), 488 (2:3), 477 (1:3).
+    int wc = 2, wb = 3;
+#ifdef GMG_EXPERIMENTS
+    if (const char* e = getenv("GMG_GS_ORDER")) sscanf(e, "%d,%d", &wc, &wb);
+#endif
+    std::stable_sort(rt.begin(), rt.end(), [wc, wb](const int2& x, const int2& y) {
+      const int kx = wc * x.x + wb * x.y, ky = wc * y.x + wb * y.y;
       return kx != ky ? kx < ky : x.x < y.x;
     });
     const uint64_t P = (uint64_t)l.g.P;

@@ -23,7 +23,7 @@ for _ in range(3):
 Nl = p.N
 C = (Nl - 1 + 15) // 16
 Bn = (Nl - 1 + 7) // 8
-tasks = sorted([(c, b) for c in range(C) for b in range(Bn)], key=lambda t: (4 * t[0] + 3 * t[1], t[0]))
+tasks = sorted([(c, b) for c in range(C) for b in range(Bn)], key=lambda t: (2 * t[0] + 3 * t[1], t[0]))
 cpl = Nl + 1 + 32
 buf = np.zeros(len(tasks) * (16 + 2 * cpl), dtype=np.int64)
 ctx.lib.gmg_debug_gs_trace(ctx.ctx, level, buf.ctypes.data, buf.size)
