@@ -271,7 +271,13 @@ static void launch_residual_march(const Geom& g, const uint8_t* labels, const do
     const int per_sm = big ? 5 : 4;
     const int64_t tk = (g.N - 1 + RM_TK - 1) / RM_TK, tj = (g.N - 1 + 8 - 1) / 8;
     const int64_t np = p_hi - p_lo + 1;
-    const int64_t segs = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, np / 4), 148 * per_sm / (tk * tj)));
+    // plane segments per tile: enough CTAs for ~7 waves of the resident slots as long as a segment keeps
+    // >= 25 planes (its ring prologue costs about six planes' time), and never fewer than one wave
+    // (512^3: 1 -> 10 segments, 679 -> 582 us; 256^3: 4 -> 10, 100 -> 95 us; smaller levels unchanged)
+    const int64_t slots = 148 * per_sm, tiles = tk * tj;
+    const int64_t one_wave = std::min<int64_t>(std::max<int64_t>(1, np / 4), slots / tiles);
+    const int64_t waves7 = std::min<int64_t>(np / 25, (7 * slots + tiles - 1) / tiles);
+    const int64_t segs = std::max<int64_t>(1, std::max(one_wave, waves7));
     dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)segs);
     if (big) {
       if (r)
@@ -602,7 +608,8 @@ void launch_restrict_interior(const Geom& gf, const double* r_f, const Geom& gc,
                               double* f_c, cudaStream_t st) {
   const int64_t inner = gc.n - 2;
   const int64_t nrows = gf.d == 3 ? inner * inner : inner;
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 8));
+  // 64 CTAs per SM's worth of rows (512^3: 320 us at 148 * 8, 303 at * 32, 295 at * 64, 341 with one CTA per row)
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, 148 * 64));
   if (gf.d == 3)
     restrict_interior_kernel<3><<<blocks, 256, 0, st>>>(gf, r_f, gc, rmask, f_c);
   else
@@ -687,7 +694,7 @@ __global__ void __launch_bounds__(256, 4) interp_add4_kernel(Geom gf, const uint
 void launch_interp_add(const Geom& gf, const uint8_t* lab_f, double* u_f, const Geom& gc,
                        const double* e_c, cudaStream_t st) {
   const int64_t nq = gf.rows * (gf.P / 4);
-  const unsigned blocks = grid_for(nq, 256, 148 * 8);
+  const unsigned blocks = grid_for(nq, 256, 148 * 8);  // 4 to 64 CTAs per SM's worth measured the same (497-503 us at 512^3)
   if (gf.d == 3)
     interp_add4_kernel<3><<<blocks, 256, 0, st>>>(gf, lab_f, u_f, gc, e_c);
   else

@@ -1,3 +1,2 @@
-for o in 4,3 2,3; do echo "== c3 order $o"; GMG_GS_ORDER=$o timeout 600 python bench.py --config c3 --no-cpu-baseline --no-e2e --no-bitexact 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['breakdown_ms_per_cycle']['gs_sweep'])"; done
-echo "== c4 default"; timeout 900 python bench.py --no-cpu-baseline --no-bitexact 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['roofline']['avg_launch_ms'], d['roofline']['frac'], d['breakdown_ms_per_cycle'], d['parity']['max_rel_diff'])"
-echo "== c5 2,3"; timeout 1500 python bench.py --config c5 --no-cpu-baseline --no-e2e --no-bitexact 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['roofline']['avg_launch_ms'], d['breakdown_ms_per_cycle']['gs_sweep'])"
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 900 python bench.py > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.log; tail -1 gpurun_out/r02_bench.json | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['e2e']['value'], d['roofline']['frac'], d['breakdown_ms_per_cycle'], d['parity']['max_rel_diff'])"
