@@ -93,7 +93,6 @@ struct DevLevel {
   int rw_ntasks = 0, rw_C = 0, rw_Bn = 0;
   double2 *bcell = nullptr, *ccell = nullptr;
   int* rw_ctl = nullptr;
-  long long* rw_hint = nullptr;
   // gs_chain.cu (3-D, production): one warp per 16-column x 8-row task, register chains; shares the
   // cell / control arrays above
   bool chain_gs = false;
@@ -181,6 +180,7 @@ struct gmg_ctx {
   int gs_chain = 1;            // 3-D levels N >= 64: gs_chain.cu (register chains; production); GMG_GS_CHAIN=0:
                                // the streaming kernel gs_stream.cu (bitwise the same results)
   
+  int gs_poll_nap = 1000;     // ns, see op_gs (GMG_GS_POLL_NAP in experiments builds)
   int gs_small = 1;            // levels with N <= 32 (3-D) / N < 64 (2-D): gs_small.cu (GMG_GS_SMALL=0: the multi-CTA
                                // kernels gs_stream.cu / gs_sweep.cu, bitwise same)
   int gs_diag = 1;             // 2-D levels N >= 64: gs_diag.cu (GMG_GS_DIAG=0: the streaming kernel, bitwise same)
@@ -289,7 +289,7 @@ void free_level(DevLevel& l) {
                   l.dep_off, l.dep, l.gctr, l.trace, l.rmask, l.vmask, l.gpair, l.ghtrace, l.dbatch_off,
                   l.bfixpos, l.bnbr, l.bv0, l.bv1, l.gwl, l.gbasel, l.gnodel, l.nd_perm, l.nd_pos, l.nd_aai, l.nd_bbi, l.nd_g,
                   l.nd_w, l.nd_si, l.nd_b_, l.nd_x, l.nd_t, l.nd_part, l.nd_crow, l.nd_ccol, l.nd_cval,
-                  l.rw_tasks, l.rw_prange, l.bcell, l.ccell, l.rw_ctl, l.rw_hint, l.pmask};  // ticket lives in progress
+                  l.rw_tasks, l.rw_prange, l.bcell, l.ccell, l.rw_ctl, l.pmask};  // ticket lives in progress
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (l.rhs_h) cudaFreeHost(l.rhs_h);
@@ -552,7 +552,8 @@ int op_gs(gmg_ctx* ctx, DevLevel& l) {
     r.ctl = l.rw_ctl;
     r.bcell = l.bcell;
     r.ccell = l.ccell;
-    r.hint = l.rw_hint;
+    // more tasks than resident CTAs (2 per SM): a pause between unproductive cell polls (gs_chain.cu)
+    r.poll_nap = l.rw_ntasks > 4 * ctx->sms ? ctx->gs_poll_nap : 0;
     r.trace = nullptr;
     if (ctx->gs_trace) {
       const int64_t tn = (int64_t)l.rw_ntasks * (16 + 2 * (l.g.n + 32));  // + per-plane hand-off stamps
@@ -1049,6 +1050,7 @@ gmg_ctx* gmg_create(int device, int ndim, int nlevels) {
   if (const char* e = getenv("GMG_GS_DIAG")) ctx->gs_diag = atoi(e);
   if (const char* e = getenv("GMG_GS_SMALL")) ctx->gs_small = atoi(e);
 #ifdef GMG_EXPERIMENTS
+  if (const char* e = getenv("GMG_GS_POLL_NAP")) ctx->gs_poll_nap = atoi(e);
   if (const char* e = getenv("GMG_SIMPLE_GS")) ctx->force_simple_gs = e[0] == '1';
   if (const char* e = getenv("GMG_NO_WS")) ctx->no_ws = e[0] == '1';
   if (const char* e = getenv("GMG_OVERLAP")) ctx->overlap = e[0] == '1';
@@ -1469,9 +1471,8 @@ int gmg_set_level(gmg_ctx* ctx, int li, int64_t N, double reaction, const uint8_
     if (upload(ctx, &l.rw_tasks, rt.data(), (int64_t)rt.size()) ||
         upload(ctx, &l.rw_prange, pr.data(), (int64_t)pr.size()) ||
         dalloc(ctx, &l.bcell, (int64_t)C * Bn * (n + 32) * W) || dalloc(ctx, &l.ccell, (int64_t)C * Bn * (n + 32) * R) ||
-        dalloc(ctx, &l.rw_ctl, 4) || dalloc(ctx, &l.rw_hint, (int64_t)C * Bn * 16) || dalloc(ctx, &l.pmask, pmw))
+        dalloc(ctx, &l.rw_ctl, 4) || dalloc(ctx, &l.pmask, pmw))
       return -1;
-    GMG_CHECK(ctx, cudaMemset(l.rw_hint, 0, sizeof(long long) * (size_t)C * Bn * 16));
     GMG_CHECK(ctx, cudaMemset(l.bcell, 0, sizeof(double2) * (size_t)C * Bn * (n + 32) * W));
     GMG_CHECK(ctx, cudaMemset(l.ccell, 0, sizeof(double2) * (size_t)C * Bn * (n + 32) * R));
     GMG_CHECK(ctx, cudaMemset(l.rw_ctl, 0, sizeof(int) * 4));

@@ -72,8 +72,8 @@ struct GsChainArgs {
   int* ctl;               // [0] sweep sequence, [1] finished CTAs, [2] ticket (zero between sweeps)
   double2* bcell;         // [c * Bn + b][cplanes][GS_CHAIN_COLS]: (value, tag) of the block's last row, per plane
   double2* ccell;         // [c * Bn + b][cplanes][GS_CHAIN_ROWS]: (value, tag) of the chunk's last column
-  long long* hint;        // [c * Bn + b][16]: progress hint (sweep << 32 | plane), one 128-byte line per task
   long long* trace;       // diagnostics: [ntasks][16] per task (ticket order), or null
+  int poll_nap;           // ns the cells warp pauses after a poll that brought nothing (0: none)
 };
 struct ChainMaps {  // boxes of gs_chain_group() planes
   CUtensorMap u;    // (P, n, n) doubles, box (GS_CHAIN_COLS + 4) x (GS_CHAIN_ROWS + 2) x G

@@ -164,14 +164,6 @@ __device__ __forceinline__ double2 cell_get(const double2* p) {
 #endif
   return v;
 }
-__device__ __forceinline__ void hint_put(long long* p, long long v) {
-  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ long long hint_get(const long long* p) {
-  long long v;
-  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -227,11 +219,6 @@ __device__ __forceinline__ void st_flag_if(int* f, int v, bool p) {
                "r"((unsigned)p)
                : "memory");
 }
-__device__ __forceinline__ void hint_put_if(long long* ptr, long long v, bool p) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.relaxed.gpu.global.b64 [%0], %1;\n}\n" ::"l"(ptr), "l"(v),
-               "r"((unsigned)p)
-               : "memory");
-}
 __device__ __forceinline__ void tma_prefetch_3d(const void* map, int x, int y, int z) {
   asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(x), "r"(y), "r"(z)
                : "memory");
@@ -264,7 +251,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
   // this sweep's cell tags: (sequence + 1) * 4096 + plane (the sequence
   // advances only after every CTA of this launch has read it)
   const int seq = *(volatile int*)a.ctl + 1;
-  const long long hseq = (long long)seq << 32;  // cell tags and progress hints of this sweep: hseq | plane
+  const long long hseq = (long long)seq << 32;  // cell tags of this sweep: hseq | plane
   // roles of the CTA's five warps: 0, 1 compute (columns 0-7 / 8-15), 2 TMA loader, 3 writer, 4 cells
   const int role = warp;
 
@@ -306,7 +293,6 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
     const double2* const bin = b > 0 ? a.bcell + (size_t)(cb - 1) * a.cplanes * CW : nullptr;
     const double2* const cin = c > 0 ? a.ccell + (size_t)(cb - a.Bn) * a.cplanes * RR : nullptr;
 #endif
-    long long* const hint_out = (bout || cout_) ? a.hint + (size_t)cb * 16 : nullptr;
     if (threadIdx.x == 0) {
       S.lready = P0 - 1;
       S.cstep[0] = 0;
@@ -770,6 +756,12 @@ __global__ void __launch_bounds__(32 * NWARPS, 2) gs_chain_kernel(GsChainArgs a,
 #if GS_CHAIN_TRACE
             ++it_hit;
 #endif
+          }
+          else if (p <= top && a.poll_nap > 0) {
+            // nothing new from the upstream task: when more tasks than CTA slots share the L2 (512^3 and up)
+            // a pause before the next poll takes 2-3 % off the sweep; on the hop-bound smaller levels it
+            // only adds latency (128^3: 157 -> 179 us with 1 us), so the host sets it per level
+            __nanosleep(a.poll_nap);
           }
 #if GS_CHAIN_ADAPT
           want = adv == want ? min(2 * want, CP) : 1;
