@@ -1,2 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 900 python bench.py > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.log; tail -1 gpurun_out/r02_bench.json | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['e2e']['value'], d['roofline']['frac'], d['roofline']['avg_launch_ms'], d['breakdown_ms_per_cycle'], d['parity']['max_rel_diff'])"
+for v in v1 v2 v3 v4; do echo "== $v"; GMG_LIB_OVERRIDE=build/exp_$v/libghostmg_b200.so timeout 600 python tools/gs_time.py c4:512 10 2>&1 | head -3; done
+echo "== base"; timeout 600 python tools/gs_time.py c4:512 10 2>&1 | head -3
